@@ -1,0 +1,245 @@
+/*
+ * ehyb_b200.h — C ABI of the B200-native EHYB SpMV path (libehyb_b200.so).
+ *
+ * Drop-in boundary for the reference package `ehyb` 0.1.0
+ * (arXiv 2204.06666, /root/reference/pkg/src/ehyb). Each entry point names
+ * the reference function it replaces (file:line). The reference is pure
+ * Python, so its "FFI" for this path is the Python API itself; the Python
+ * shim in paper_2204_06666_b200/ binds these symbols with ctypes and keeps
+ * the reference's signatures, dataclasses and error wording
+ * (see INTEGRATION.md for the binding a maintainer would add to `ehyb`).
+ *
+ * Conventions
+ *  - Every function returns 0 on success. A nonzero return is an error whose
+ *    message (the reference's ValueError wording where one exists) is
+ *    available from ehyb_last_error() on the calling thread:
+ *      EHYB_EINVAL (1)  -> ValueError in Python
+ *      EHYB_ENOMEM (2)  -> MemoryError
+ *      EHYB_ECUDA  (3)  -> RuntimeError (CUDA / cuSPARSE failure)
+ *  - Plain pointers and sizes only; no caller pointer is retained past the
+ *    call except by a device handle, which owns device copies of the matrix
+ *    (uploaded once in ehyb_dev_create, freed by ehyb_dev_destroy).
+ *  - Arrays the library allocates (marked "lib-alloc") are released with
+ *    ehyb_free().
+ *  - Device entry points take CUDA device pointers and a cudaStream_t passed
+ *    as void*; launches are stream-ordered and never synchronise the host
+ *    unless stated.
+ */
+#ifndef EHYB_B200_H
+#define EHYB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EHYB_API __attribute__((visibility("default")))
+
+#define EHYB_EINVAL 1
+#define EHYB_ENOMEM 2
+#define EHYB_ECUDA 3
+
+#define EHYB_MAX_LOCAL_INDEX 65536 /* format.py:21 MAX_LOCAL_INDEX */
+
+/* SpMV arithmetic modes */
+#define EHYB_MODE_STRICT 0 /* separately rounded mul + add, k ascending: bitwise == reference */
+#define EHYB_MODE_FMA 1    /* fused multiply-add; within 1e-12 (fp64) / 1e-5 (fp32) */
+
+/* ------------------------------------------------------------ utilities */
+EHYB_API const char* ehyb_last_error(void);
+EHYB_API int ehyb_abi_version(void); /* bumps on any signature change */
+EHYB_API void ehyb_free(void* p);
+EHYB_API int ehyb_num_threads(void); /* OpenMP threads used by host preprocessing */
+
+/* ------------------------------------------------- host preprocessing */
+
+/* compute_params (format.py:83-107, Eq.1-2): smallest k with the
+ * warp-aligned window vec = align_up(ceil(dimension/(k*procs)), warp)
+ * satisfying vec*tau <= shm and vec <= 65536. */
+EHYB_API int ehyb_compute_params(int64_t dimension, int32_t tau, int64_t procs, int64_t warp,
+                                 int64_t shm, int64_t* out_k, int64_t* out_n_parts,
+                                 int64_t* out_vec);
+
+/* build_graph (partition.py:77-98): symmetrised off-diagonal adjacency,
+ * sorted duplicate-free neighbour lists. adj_ptr: caller-alloc int64[n+1];
+ * *out_adj: lib-alloc int32[*out_n_adj]. */
+EHYB_API int ehyb_build_graph(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                              int64_t* adj_ptr, int32_t** out_adj, int64_t* out_n_adj);
+
+/* partition_graph (partition.py:101-204): BFS region growing seeded at
+ * min-degree vertices (CPython random.Random(seed) tie draws), leftover
+ * regions, round-robin isolated vertices, one refinement pass.
+ * assignment: caller-alloc int64[n]; sizes: caller-alloc int64[n_parts]. */
+EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32_t* adj,
+                                  int64_t n_parts, int64_t capacity, int64_t seed,
+                                  int64_t* assignment, int64_t* sizes);
+
+/* rebalance_partition (partition.py:224-262). */
+EHYB_API int ehyb_rebalance_partition(int64_t n, const int64_t* adj_ptr, const int32_t* adj,
+                                      int64_t n_parts, int64_t capacity,
+                                      const int64_t* assignment_in, int64_t* assignment,
+                                      int64_t* sizes);
+
+/* classify_rows (format.py:123-137). inner/outer/row_order: caller-alloc
+ * int64[n]; *out_er_row_order: lib-alloc int64[*out_n_er]. */
+EHYB_API int ehyb_classify_rows(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                                const int64_t* assignment, int64_t n_parts, int64_t* inner,
+                                int64_t* outer, int64_t* row_order, int64_t** out_er_row_order,
+                                int64_t* out_n_er);
+
+/* build_reorder_plan (format.py:161-199). reorder/inverse: int64[n_parts*vec];
+ * arrange: int64[n]; y_idx_er: int64[n_er]; all caller-alloc. */
+EHYB_API int ehyb_build_reorder_plan(int64_t n, int64_t n_parts, int64_t vec,
+                                     const int64_t* assignment, const int64_t* part_sizes,
+                                     const int64_t* row_order, const int64_t* er_row_order,
+                                     int64_t n_er, int64_t* reorder, int64_t* inverse,
+                                     int64_t* arrange, int64_t* y_idx_er);
+
+/* assemble_ehyb (format.py:302-409). Caller-alloc (sizes known up front):
+ * position_ell i32[padded/warp+1], width_ell i32[padded/warp],
+ * ell_row_widths i32[padded], part_boundary i32[n_parts+1],
+ * position_er i32[ceil(n_er/warp)+1], width_er i32[ceil(n_er/warp)],
+ * er_row_widths i32[n_er]. Lib-alloc: val_ell (f32|f64)[slots_ell],
+ * col_ell u16[slots_ell], val_er (f32|f64)[slots_er], col_er u32[slots_er]. */
+EHYB_API int ehyb_assemble(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                           const double* values, const int64_t* assignment,
+                           const int64_t* reorder, const int64_t* arrange, int64_t n_er,
+                           int64_t warp, int64_t vec, int64_t n_parts, int32_t tau,
+                           int32_t* position_ell, int32_t* width_ell, int32_t* ell_row_widths,
+                           int32_t* part_boundary, int32_t* position_er, int32_t* width_er,
+                           int32_t* er_row_widths, void** out_val_ell, uint16_t** out_col_ell,
+                           int64_t* out_slots_ell, void** out_val_er, uint32_t** out_col_er,
+                           int64_t* out_slots_er);
+
+/* Host view of an assembled EhybMatrix (format.py:202-248). Array lengths
+ * travel beside their pointers so ehyb_check can validate them. */
+typedef struct ehyb_host_matrix {
+  int64_t dimension;
+  int64_t padded_dimension;
+  int64_t plan_padded_dimension;
+  int64_t k;
+  int64_t n_parts;
+  int64_t vec_cache_size;
+  int64_t warp_size;
+  int64_t tau;
+  int64_t n_er_rows;
+  const int64_t* reorder; int64_t n_reorder;
+  const int64_t* inverse; int64_t n_inverse;
+  const int64_t* y_idx_er; int64_t n_y_idx_er;
+  const int32_t* part_boundary; int64_t n_part_boundary;
+  const int32_t* position_ell; int64_t n_position_ell;
+  const int32_t* width_ell; int64_t n_width_ell;
+  const int32_t* ell_row_widths; int64_t n_ell_row_widths;
+  const uint16_t* col_ell; int64_t n_col_ell;
+  const void* val_ell; int64_t slots_ell;
+  const int32_t* position_er; int64_t n_position_er;
+  const int32_t* width_er; int64_t n_width_er;
+  const int32_t* er_row_widths; int64_t n_er_row_widths;
+  const uint32_t* col_er; int64_t n_col_er;
+  const void* val_er; int64_t slots_er;
+} ehyb_host_matrix;
+
+/* EhybMatrix.check (format.py:250-299): structural invariants, O(size). */
+EHYB_API int ehyb_check(const ehyb_host_matrix* m);
+
+/* ------------------------------------------------------ device (B200) */
+
+typedef struct ehyb_dev ehyb_dev; /* opaque device handle */
+
+typedef struct ehyb_dev_info {
+  int64_t device_bytes;       /* total HBM held by the handle */
+  int64_t er_slices;          /* per-partition ER slices (derived layout) */
+  int64_t er_slots;           /* derived ER slots incl. padding */
+  int64_t window_bytes;       /* x window staged per CTA */
+  int32_t window_in_smem;     /* 1: window staged in shared memory by TMA bulk copy */
+  int32_t threads_per_cta;
+  int32_t ctas;               /* grid size of one SpMV launch */
+  int32_t sm_count;
+} ehyb_dev_info;
+
+/* Upload an assembled matrix once (device = CUDA ordinal) and derive the
+ * per-partition ER layout the fused kernel reads. Replaces the per-call
+ * array traversal of spmv_ehyb (engine.py:108-216). */
+EHYB_API int ehyb_dev_create(const ehyb_host_matrix* m, int device, ehyb_dev** out);
+EHYB_API int ehyb_dev_destroy(ehyb_dev* h);
+EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
+
+/* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].
+ * x, y: device arrays of the stored precision (tau 4 -> float, 8 -> double),
+ * non-aliasing. One fused kernel: per partition, TMA-staged x window ->
+ * ELL slices -> the partition's ER rows. mode: EHYB_MODE_*. */
+EHYB_API int ehyb_dev_spmv(ehyb_dev* h, const void* x_dev, void* y_dev, int mode, void* stream);
+
+/* permute_vector (format.py:445-452) / unpermute_vector (format.py:455-460)
+ * on device; x_user, y_user have `dimension` entries, x_r / y_r padded. */
+EHYB_API int ehyb_dev_permute(ehyb_dev* h, const void* x_user, void* x_r, void* stream);
+EHYB_API int ehyb_dev_unpermute(ehyb_dev* h, const void* y_r, void* y_user, void* stream);
+
+/* spmv_ehyb_user (engine.py:219-227) on device buffers in user order:
+ * permute -> fused SpMV -> unpermute, using handle-owned scratch. */
+EHYB_API int ehyb_dev_spmv_user(ehyb_dev* h, const void* x_user, void* y_user, int mode,
+                                void* stream);
+
+/* The same from HOST memory: copy x in, run, copy y out, synchronise.
+ * user_order=1: x,y have `dimension` entries (spmv_ehyb_user);
+ * user_order=0: x,y are padded reordered vectors (spmv_ehyb).
+ * Host buffers may be pageable or pinned (pinned is faster). */
+EHYB_API int ehyb_dev_spmv_host(ehyb_dev* h, const void* x_host, void* y_host, int user_order,
+                                int mode, void* stream);
+
+/* ------------------------------------------- cuSPARSE CSR comparator */
+typedef struct ehyb_csr ehyb_csr;
+/* CSR (coo_to_csr, matrix_io.py:255-268 layout) uploaded with int32 indices
+ * and values at tau bytes. */
+EHYB_API int ehyb_csr_create(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                             const int64_t* col_idx, const double* values, int32_t tau,
+                             int device, ehyb_csr** out);
+/* y = A x with cusparseSpMV; alg 1 = CUSPARSE_SPMV_CSR_ALG1, 2 = ALG2. */
+EHYB_API int ehyb_csr_spmv(ehyb_csr* h, const void* x_dev, void* y_dev, int alg, void* stream);
+EHYB_API int ehyb_csr_destroy(ehyb_csr* h);
+
+/* --------------------------------------------- multi-GPU row shards */
+
+/* A shard owns a contiguous block of partitions [p0, p1) of a matrix that
+ * was assembled once for the whole job; its x/y range is the new-row range
+ * [p0*vec, p1*vec). ER columns outside that range are remapped into a halo
+ * segment appended after the owned window: x_ext = [owned | halo]. */
+typedef struct ehyb_shard_plan {
+  int64_t p0, p1;          /* owned partitions */
+  int64_t n_halo;          /* distinct remote columns referenced by owned ER rows */
+  const int64_t* halo_cols;/* global new-order column of each halo slot (ascending) */
+} ehyb_shard_plan;
+
+/* Upload the owned part of the matrix; ER columns are remapped against
+ * plan->halo_cols. The shard's SpMV reads x_ext[(p1-p0)*vec + n_halo]. */
+EHYB_API int ehyb_dev_create_shard(const ehyb_host_matrix* m, const ehyb_shard_plan* plan,
+                                   int device, ehyb_dev** out);
+
+/* Split SpMV for overlap with the halo exchange: the ELL phase needs only
+ * owned x; the ER phase needs x_ext complete. ehyb_dev_spmv on a shard
+ * handle runs both back to back. */
+EHYB_API int ehyb_dev_spmv_ell(ehyb_dev* h, const void* x_ext, void* y_local, int mode,
+                               void* stream);
+EHYB_API int ehyb_dev_spmv_er(ehyb_dev* h, const void* x_ext, void* y_local, int mode,
+                              void* stream);
+
+/* Gather x_local[idx[i]] into a packed send buffer (halo pack). */
+EHYB_API int ehyb_dev_gather(const void* src, const int64_t* idx_dev, int64_t count, void* dst,
+                             int32_t tau, void* stream);
+
+/* ------------------------------------------------ CG building blocks */
+/* dot products of the CG loop, accumulated in fp64 into out_dev[0]
+ * (deterministic two-level reduction, no atomics). */
+EHYB_API int ehyb_dev_dot(const void* a, const void* b, int64_t n, int32_t tau, double* out_dev,
+                          void* stream);
+/* y = a*x + y (a read from device memory, scaled by sign). */
+EHYB_API int ehyb_dev_axpy(const double* a_dev, double sign, const void* x, void* y, int64_t n,
+                           int32_t tau, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EHYB_B200_H */

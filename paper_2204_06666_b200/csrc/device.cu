@@ -1,0 +1,644 @@
+// Device side of the C ABI: matrix upload (ehyb_dev_create / _create_shard),
+// the derived per-partition ER layout, SpMV launches, permutation, the
+// cuSPARSE comparator and the CG vector primitives.
+//
+// Derived layout (built once at upload, never a parity object): the
+// reference stores ER rows globally sorted by outer count and sliced by
+// warp_size (format.py:367-392); its engine runs them after a grid-wide
+// barrier (engine.py:146-154, 172-173). Here the ER rows are regrouped by
+// the partition that owns their output row (y_idx_er // vec), keeping the
+// reference's relative order (so widths stay descending) and re-sliced in
+// 32-row SELL slices, so the owning CTA finishes its own rows without a
+// grid barrier or atomics. Each row keeps its entries in the reference's k
+// order, so the accumulation is unchanged.
+
+#include "ehyb_common.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <cusparse.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+using namespace ehyb;
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t err__ = (expr);                                                              \
+    if (err__ != cudaSuccess)                                                                \
+      return ehyb::fail(std::string(#expr) + ": " + cudaGetErrorString(err__), EHYB_ECUDA); \
+  } while (0)
+
+#define CUSPARSE_TRY(expr)                                                                 \
+  do {                                                                                     \
+    cusparseStatus_t st__ = (expr);                                                        \
+    if (st__ != CUSPARSE_STATUS_SUCCESS)                                                   \
+      return ehyb::fail(std::string(#expr) + ": cusparse status " + std::to_string(int(st__)), \
+                        EHYB_ECUDA);                                                       \
+  } while (0)
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename P>
+cudaError_t upload(P** dst, const void* src, size_t bytes, size_t* total) {
+  *dst = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) return e;
+  *total += std::max<size_t>(bytes, 16);
+  if (bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  return e;
+}
+
+}  // namespace
+
+struct ehyb_dev {
+  int device = 0;
+  int tau = 8;
+  int64_t dimension = 0, padded = 0, n_parts = 0, vec = 0, warp = 32;
+  int64_t local_rows = 0, n_halo = 0;  // shard geometry (full matrix: local_rows == padded)
+  bool shard = false;
+  // ELL parity arrays (re-based to the owned partitions)
+  void* val_ell = nullptr;
+  uint16_t* col_ell = nullptr;
+  int32_t* pos_ell = nullptr;
+  int32_t* width_ell = nullptr;
+  // derived ER
+  int64_t er_slices = 0, er_slots = 0;
+  int32_t* er_part_ptr = nullptr;
+  int64_t* er_pos = nullptr;
+  int32_t* er_swidth = nullptr;
+  int32_t* er_rows = nullptr;
+  int32_t* er_lwidth = nullptr;
+  void* er_val = nullptr;
+  uint32_t* er_col = nullptr;
+  // permutation (full matrix only)
+  int32_t* reorder = nullptr;  // [dimension]
+  int32_t* inverse = nullptr;  // [padded]
+  // scratch
+  void* xr = nullptr;
+  void* yr = nullptr;
+  void* xu = nullptr;
+  void* yu = nullptr;
+  // launch configuration
+  int threads = 1024;
+  size_t smem = 0;
+  bool window_in_smem = false, window_tma = false;
+  int sm_count = 0;
+  size_t bytes = 0;
+
+  ~ehyb_dev() {
+    void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
+                    er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+
+template <typename T, bool STRICT, bool C32>
+cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell, bool do_er,
+                         cudaStream_t st) {
+  SpmvParams<T> P;
+  P.val_ell = static_cast<const T*>(h->val_ell);
+  P.col_ell = h->col_ell;
+  P.pos_ell = h->pos_ell;
+  P.width_ell = h->width_ell;
+  P.er_part_ptr = h->er_part_ptr;
+  P.er_pos = h->er_pos;
+  P.er_swidth = h->er_swidth;
+  P.er_rows = h->er_rows;
+  P.er_lwidth = h->er_lwidth;
+  P.er_val = static_cast<const T*>(h->er_val);
+  P.er_col = h->er_col;
+  P.x = static_cast<const T*>(x);
+  P.y = static_cast<T*>(y);
+  P.vec = h->vec;
+  P.warp = int32_t(h->warp);
+  P.window_in_smem = (do_ell && h->window_in_smem) ? 1 : 0;
+  P.window_tma = h->window_tma ? 1 : 0;
+  P.do_ell = do_ell ? 1 : 0;
+  P.do_er = do_er ? 1 : 0;
+  auto kern = spmv_fused_kernel<T, STRICT, C32>;
+  const size_t smem = P.window_in_smem ? h->smem : 0;
+  if (smem > 48 * 1024) {
+    // opt in once per (kernel, device) to the largest window any handle needs
+    static std::mutex mu;
+    static std::unordered_map<std::string, size_t> configured;
+    const std::string key = std::to_string(reinterpret_cast<uintptr_t>(
+                                reinterpret_cast<const void*>(kern))) + ":" + std::to_string(h->device);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = configured.find(key);
+    if (it == configured.end() || it->second < smem) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      configured[key] = smem;
+    }
+  }
+  const int64_t n_local_parts = h->local_rows / h->vec;
+  kern<<<dim3(unsigned(n_local_parts)), dim3(unsigned(h->threads)), smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
+                        cudaStream_t st) {
+  const bool c32 = h->warp == 32;
+  if (mode == EHYB_MODE_FMA)
+    return c32 ? launch_typed<T, false, true>(h, x, y, ell, er, st)
+               : launch_typed<T, false, false>(h, x, y, ell, er, st);
+  return c32 ? launch_typed<T, true, true>(h, x, y, ell, er, st)
+             : launch_typed<T, true, false>(h, x, y, ell, er, st);
+}
+
+cudaError_t launch_spmv(const ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
+                        cudaStream_t st) {
+  return h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
+                     : launch_mode<double>(h, x, y, mode, ell, er, st);
+}
+
+int grid_for(int64_t n, int threads, int sms) {
+  int64_t g = (n + threads - 1) / threads;
+  return int(std::max<int64_t>(1, std::min<int64_t>(g, int64_t(sms) * 16)));
+}
+
+// Build the device copy of partitions [p0, p1). ER columns are remapped:
+// owned columns -> c - p0*vec, halo columns -> local_rows + slot in halo_cols.
+int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t* halo_cols,
+                int64_t n_halo, bool shard, int device, ehyb_dev** out) {
+  if (!m || !out) return fail("null argument");
+  if (m->tau != 4 && m->tau != 8) return fail("tau must be 4 or 8");
+  if (p0 < 0 || p1 > m->n_parts || p0 >= p1) return fail("bad shard partition range");
+  const int64_t vec = m->vec_cache_size, C = m->warp_size;
+  const int64_t padded = m->padded_dimension;
+  if (padded >= (int64_t(1) << 30)) return fail("padded dimension exceeds the 2^30 device row range");
+  const size_t tb = size_t(m->tau);
+
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail("invalid CUDA device ordinal", EHYB_ECUDA);
+  DeviceGuard guard(device);
+  auto h = std::make_unique<ehyb_dev>();
+  h->device = device;
+  h->tau = int(m->tau);
+  h->dimension = m->dimension;
+  h->padded = padded;
+  h->n_parts = m->n_parts;
+  h->vec = vec;
+  h->warp = C;
+  h->shard = shard;
+  h->local_rows = (p1 - p0) * vec;
+  h->n_halo = n_halo;
+  const int64_t row_lo = p0 * vec, row_hi = p1 * vec;
+
+  // ---- ELL: slices of the owned rows, positions re-based
+  const int64_t s_lo = row_lo / C, s_hi = row_hi / C;
+  const int64_t base = m->position_ell[s_lo];
+  const int64_t slots = int64_t(m->position_ell[s_hi]) - base;
+  std::vector<int32_t> pos(size_t(s_hi - s_lo) + 1);
+  for (int64_t s = s_lo; s <= s_hi; ++s) pos[size_t(s - s_lo)] = int32_t(m->position_ell[s] - base);
+  CUDA_TRY(upload(&h->pos_ell, pos.data(), pos.size() * 4, &h->bytes));
+  CUDA_TRY(upload(&h->width_ell, m->width_ell + s_lo, size_t(s_hi - s_lo) * 4, &h->bytes));
+  CUDA_TRY(upload(&h->val_ell, static_cast<const char*>(m->val_ell) + size_t(base) * tb,
+                  size_t(slots) * tb, &h->bytes));
+  CUDA_TRY(upload(&h->col_ell, m->col_ell + base, size_t(slots) * 2, &h->bytes));
+
+  // ---- ER regrouped per owning partition
+  const int64_t n_loc_parts = p1 - p0;
+  std::vector<std::vector<int64_t>> members(static_cast<size_t>(n_loc_parts));
+  for (int64_t j = 0; j < m->n_er_rows; ++j) {
+    const int64_t r = m->y_idx_er[j];
+    if (r >= row_lo && r < row_hi) members[size_t(r / vec - p0)].push_back(j);
+  }
+  std::unordered_map<int64_t, int64_t> halo_index;
+  halo_index.reserve(size_t(n_halo) * 2 + 1);
+  for (int64_t i = 0; i < n_halo; ++i) halo_index[halo_cols[i]] = h->local_rows + i;
+  std::vector<int32_t> part_ptr(size_t(n_loc_parts) + 1, 0);
+  for (int64_t q = 0; q < n_loc_parts; ++q)
+    part_ptr[size_t(q) + 1] = part_ptr[size_t(q)] + int32_t((members[size_t(q)].size() + 31) / 32);
+  const int64_t n_sl = part_ptr[size_t(n_loc_parts)];
+  std::vector<int64_t> epos(size_t(n_sl) + 1, 0);
+  std::vector<int32_t> eswidth(size_t(n_sl), 0), erows(size_t(n_sl) * 32, -1),
+      elwidth(size_t(n_sl) * 32, 0);
+  for (int64_t q = 0; q < n_loc_parts; ++q) {
+    const auto& mem = members[size_t(q)];
+    for (size_t i = 0; i < mem.size(); ++i) {
+      const int64_t j = mem[i];
+      const int64_t sl = part_ptr[size_t(q)] + int64_t(i / 32);
+      const int32_t w = m->er_row_widths[j];
+      const int64_t ref_w = m->width_er[j / C];
+      int32_t row = int32_t(m->y_idx_er[j] - row_lo);
+      if (!shard && w < ref_w) row |= kPadFlag;
+      erows[size_t(sl) * 32 + i % 32] = row;
+      elwidth[size_t(sl) * 32 + i % 32] = w;
+      eswidth[size_t(sl)] = std::max(eswidth[size_t(sl)], w);
+    }
+  }
+  for (int64_t s = 0; s < n_sl; ++s) epos[size_t(s) + 1] = epos[size_t(s)] + 32 * int64_t(eswidth[size_t(s)]);
+  const int64_t eslots = epos[size_t(n_sl)];
+  std::vector<char> evals(size_t(std::max<int64_t>(eslots, 1)) * tb, 0);
+  std::vector<uint32_t> ecols(size_t(std::max<int64_t>(eslots, 1)), 0);
+  for (int64_t q = 0; q < n_loc_parts; ++q) {
+    const auto& mem = members[size_t(q)];
+    for (size_t i = 0; i < mem.size(); ++i) {
+      const int64_t j = mem[i];
+      const int64_t sl = part_ptr[size_t(q)] + int64_t(i / 32);
+      const int64_t w = m->er_row_widths[j];
+      const int64_t src0 = int64_t(m->position_er[j / C]) + j % C;
+      const int64_t dst0 = epos[size_t(sl)] + int64_t(i % 32);
+      for (int64_t k = 0; k < w; ++k) {
+        const int64_t src = src0 + k * C, dst = dst0 + k * 32;
+        std::memcpy(&evals[size_t(dst) * tb], static_cast<const char*>(m->val_er) + size_t(src) * tb, tb);
+        const int64_t c = m->col_er[src];
+        int64_t lc;
+        if (c >= row_lo && c < row_hi) {
+          lc = c - row_lo;
+        } else {
+          auto it = halo_index.find(c);
+          if (it == halo_index.end()) return fail("ER column missing from the shard halo plan");
+          lc = it->second;
+        }
+        ecols[size_t(dst)] = uint32_t(lc);
+      }
+    }
+  }
+  h->er_slices = n_sl;
+  h->er_slots = eslots;
+  CUDA_TRY(upload(&h->er_part_ptr, part_ptr.data(), part_ptr.size() * 4, &h->bytes));
+  CUDA_TRY(upload(&h->er_pos, epos.data(), epos.size() * 8, &h->bytes));
+  CUDA_TRY(upload(&h->er_swidth, eswidth.data(), eswidth.size() * 4, &h->bytes));
+  CUDA_TRY(upload(&h->er_rows, erows.data(), erows.size() * 4, &h->bytes));
+  CUDA_TRY(upload(&h->er_lwidth, elwidth.data(), elwidth.size() * 4, &h->bytes));
+  CUDA_TRY(upload(&h->er_val, evals.data(), size_t(eslots) * tb, &h->bytes));
+  CUDA_TRY(upload(&h->er_col, ecols.data(), size_t(eslots) * 4, &h->bytes));
+
+  // ---- permutation tables (int32) for the user-order entry points
+  if (!shard) {
+    std::vector<int32_t> ro(static_cast<size_t>(m->dimension)), inv(static_cast<size_t>(padded));
+    for (int64_t i = 0; i < m->dimension; ++i) ro[size_t(i)] = int32_t(m->reorder[i]);
+    for (int64_t i = 0; i < padded; ++i) inv[size_t(i)] = int32_t(m->inverse[i]);
+    CUDA_TRY(upload(&h->reorder, ro.data(), ro.size() * 4, &h->bytes));
+    CUDA_TRY(upload(&h->inverse, inv.data(), inv.size() * 4, &h->bytes));
+  }
+
+  // ---- launch configuration
+  int optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  CUDA_TRY(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
+  const size_t win = size_t(vec) * tb;
+  const size_t win_al = (win + 127) / 128 * 128;
+  h->window_in_smem = win_al + 64 <= size_t(optin);
+  h->smem = h->window_in_smem ? win_al : 0;
+  // TMA bulk copies need 16-byte aligned source offsets and sizes
+  h->window_tma = h->window_in_smem && (win % 16 == 0);
+  const int64_t chunks = (vec + 31) / 32;
+  h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(32, chunks * 32)));
+  *out = h.release();
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+EHYB_API int ehyb_dev_create(const ehyb_host_matrix* m, int device, ehyb_dev** out) {
+  EHYB_TRY {
+    int rc = ehyb_check(m);
+    if (rc) return rc;
+    return create_impl(m, 0, m->n_parts, nullptr, 0, false, device, out);
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_create_shard(const ehyb_host_matrix* m, const ehyb_shard_plan* plan,
+                                   int device, ehyb_dev** out) {
+  EHYB_TRY {
+    if (!plan) return fail("null shard plan");
+    int rc = ehyb_check(m);
+    if (rc) return rc;
+    return create_impl(m, plan->p0, plan->p1, plan->halo_cols, plan->n_halo, true, device, out);
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_destroy(ehyb_dev* h) {
+  if (!h) return 0;
+  DeviceGuard guard(h->device);
+  delete h;
+  return 0;
+}
+
+EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out) {
+  if (!h || !out) return fail("null argument");
+  out->device_bytes = int64_t(h->bytes);
+  out->er_slices = h->er_slices;
+  out->er_slots = h->er_slots;
+  out->window_bytes = h->vec * h->tau;
+  out->window_in_smem = h->window_in_smem ? 1 : 0;
+  out->threads_per_cta = h->threads;
+  out->ctas = int32_t(h->local_rows / h->vec);
+  out->sm_count = h->sm_count;
+  return 0;
+}
+
+EHYB_API int ehyb_dev_spmv(ehyb_dev* h, const void* x_dev, void* y_dev, int mode, void* stream) {
+  EHYB_TRY {
+    if (!h || !x_dev || !y_dev) return fail("null argument");
+    if (x_dev == y_dev) return fail("x and y must not alias");
+    DeviceGuard guard(h->device);
+    CUDA_TRY(launch_spmv(h, x_dev, y_dev, mode, true, true, static_cast<cudaStream_t>(stream)));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_spmv_ell(ehyb_dev* h, const void* x_ext, void* y_local, int mode,
+                               void* stream) {
+  EHYB_TRY {
+    if (!h || !x_ext || !y_local) return fail("null argument");
+    DeviceGuard guard(h->device);
+    CUDA_TRY(launch_spmv(h, x_ext, y_local, mode, true, false, static_cast<cudaStream_t>(stream)));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_spmv_er(ehyb_dev* h, const void* x_ext, void* y_local, int mode,
+                              void* stream) {
+  EHYB_TRY {
+    if (!h || !x_ext || !y_local) return fail("null argument");
+    DeviceGuard guard(h->device);
+    CUDA_TRY(launch_spmv(h, x_ext, y_local, mode, false, true, static_cast<cudaStream_t>(stream)));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_permute(ehyb_dev* h, const void* x_user, void* x_r, void* stream) {
+  EHYB_TRY {
+    if (!h || h->shard) return fail("permute needs a full-matrix handle");
+    DeviceGuard guard(h->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    const int g = grid_for(h->padded, 256, h->sm_count);
+    if (h->tau == 4)
+      permute_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(x_user), h->inverse,
+                                                h->dimension, h->padded, static_cast<float*>(x_r));
+    else
+      permute_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(x_user), h->inverse,
+                                                 h->dimension, h->padded, static_cast<double*>(x_r));
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_unpermute(ehyb_dev* h, const void* y_r, void* y_user, void* stream) {
+  EHYB_TRY {
+    if (!h || h->shard) return fail("unpermute needs a full-matrix handle");
+    DeviceGuard guard(h->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    const int g = grid_for(h->dimension, 256, h->sm_count);
+    if (h->tau == 4)
+      unpermute_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(y_r), h->reorder,
+                                                  h->dimension, static_cast<float*>(y_user));
+    else
+      unpermute_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(y_r), h->reorder,
+                                                   h->dimension, static_cast<double*>(y_user));
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+static int ensure_scratch(ehyb_dev* h) {
+  const size_t tb = size_t(h->tau);
+  if (!h->xr) {
+    CUDA_TRY(cudaMalloc(&h->xr, size_t(h->padded) * tb));
+    CUDA_TRY(cudaMalloc(&h->yr, size_t(h->padded) * tb));
+    CUDA_TRY(cudaMalloc(&h->xu, std::max<size_t>(size_t(h->dimension) * tb, 16)));
+    CUDA_TRY(cudaMalloc(&h->yu, std::max<size_t>(size_t(h->dimension) * tb, 16)));
+    h->bytes += 2 * size_t(h->padded) * tb + 2 * size_t(h->dimension) * tb;
+  }
+  return 0;
+}
+
+EHYB_API int ehyb_dev_spmv_user(ehyb_dev* h, const void* x_user, void* y_user, int mode,
+                                void* stream) {
+  EHYB_TRY {
+    if (!h || h->shard) return fail("spmv_user needs a full-matrix handle");
+    DeviceGuard guard(h->device);
+    int rc = ensure_scratch(h);
+    if (rc) return rc;
+    rc = ehyb_dev_permute(h, x_user, h->xr, stream);
+    if (rc) return rc;
+    CUDA_TRY(launch_spmv(h, h->xr, h->yr, mode, true, true, static_cast<cudaStream_t>(stream)));
+    return ehyb_dev_unpermute(h, h->yr, y_user, stream);
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_spmv_host(ehyb_dev* h, const void* x_host, void* y_host, int user_order,
+                                int mode, void* stream) {
+  EHYB_TRY {
+    if (!h || h->shard) return fail("spmv_host needs a full-matrix handle");
+    DeviceGuard guard(h->device);
+    int rc = ensure_scratch(h);
+    if (rc) return rc;
+    auto st = static_cast<cudaStream_t>(stream);
+    const size_t tb = size_t(h->tau);
+    if (user_order) {
+      const size_t nb = size_t(h->dimension) * tb;
+      CUDA_TRY(cudaMemcpyAsync(h->xu, x_host, nb, cudaMemcpyHostToDevice, st));
+      rc = ehyb_dev_spmv_user(h, h->xu, h->yu, mode, stream);
+      if (rc) return rc;
+      CUDA_TRY(cudaMemcpyAsync(y_host, h->yu, nb, cudaMemcpyDeviceToHost, st));
+    } else {
+      const size_t pb = size_t(h->padded) * tb;
+      CUDA_TRY(cudaMemcpyAsync(h->xr, x_host, pb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(launch_spmv(h, h->xr, h->yr, mode, true, true, st));
+      CUDA_TRY(cudaMemcpyAsync(y_host, h->yr, pb, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_gather(const void* src, const int64_t* idx_dev, int64_t count, void* dst,
+                             int32_t tau, void* stream) {
+  EHYB_TRY {
+    if (count <= 0) return 0;
+    auto st = static_cast<cudaStream_t>(stream);
+    const int g = int(std::min<int64_t>((count + 255) / 256, 148 * 16));
+    if (tau == 4)
+      gather_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(src), idx_dev, count,
+                                               static_cast<float*>(dst));
+    else
+      gather_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(src), idx_dev, count,
+                                                static_cast<double*>(dst));
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_dot(const void* a, const void* b, int64_t n, int32_t tau, double* out_dev,
+                          void* stream) {
+  EHYB_TRY {
+    auto st = static_cast<cudaStream_t>(stream);
+    constexpr int kBlocks = 592, kThreads = 512;
+    static thread_local std::unordered_map<int, double*> partials;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    double*& part = partials[dev];
+    if (!part) CUDA_TRY(cudaMalloc(&part, kBlocks * sizeof(double)));
+    if (tau == 4)
+      dot_partial_kernel<float><<<kBlocks, kThreads, 0, st>>>(
+          static_cast<const float*>(a), static_cast<const float*>(b), n, part);
+    else
+      dot_partial_kernel<double><<<kBlocks, kThreads, 0, st>>>(
+          static_cast<const double*>(a), static_cast<const double*>(b), n, part);
+    dot_final_kernel<<<1, 1024, 0, st>>>(part, kBlocks, out_dev);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_axpy(const double* a_dev, double sign, const void* x, void* y, int64_t n,
+                           int32_t tau, void* stream) {
+  EHYB_TRY {
+    auto st = static_cast<cudaStream_t>(stream);
+    const int g = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+    if (tau == 4)
+      axpy_kernel<float><<<g, 256, 0, st>>>(a_dev, sign, static_cast<const float*>(x),
+                                             static_cast<float*>(y), n);
+    else
+      axpy_kernel<double><<<g, 256, 0, st>>>(a_dev, sign, static_cast<const double*>(x),
+                                              static_cast<double*>(y), n);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ cuSPARSE CSR
+struct ehyb_csr {
+  int device = 0;
+  int tau = 8;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int32_t* row_ptr = nullptr;
+  int32_t* col_idx = nullptr;
+  void* vals = nullptr;
+  void* buffer = nullptr;
+  size_t buffer_bytes = 0;
+  cusparseHandle_t handle = nullptr;
+  cusparseSpMatDescr_t mat = nullptr;
+  ~ehyb_csr() {
+    if (mat) cusparseDestroySpMat(mat);
+    if (handle) cusparseDestroy(handle);
+    void* ptrs[] = {row_ptr, col_idx, vals, buffer};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+EHYB_API int ehyb_csr_create(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                             const int64_t* col_idx, const double* values, int32_t tau,
+                             int device, ehyb_csr** out) {
+  EHYB_TRY {
+    if (nnz >= (int64_t(1) << 31)) return fail("CSR comparator needs nnz < 2^31");
+    DeviceGuard guard(device);
+    auto h = std::make_unique<ehyb_csr>();
+    h->device = device;
+    h->tau = tau;
+    h->n_rows = n_rows;
+    h->n_cols = n_cols;
+    h->nnz = nnz;
+    std::vector<int32_t> rp(size_t(n_rows) + 1), ci(size_t(std::max<int64_t>(nnz, 1)));
+    for (int64_t i = 0; i <= n_rows; ++i) rp[size_t(i)] = int32_t(row_ptr[i]);
+    for (int64_t i = 0; i < nnz; ++i) ci[size_t(i)] = int32_t(col_idx[i]);
+    size_t total = 0;
+    CUDA_TRY(upload(&h->row_ptr, rp.data(), rp.size() * 4, &total));
+    CUDA_TRY(upload(&h->col_idx, ci.data(), size_t(nnz) * 4, &total));
+    if (tau == 4) {
+      std::vector<float> v(size_t(std::max<int64_t>(nnz, 1)));
+      for (int64_t i = 0; i < nnz; ++i) v[size_t(i)] = float(values[i]);
+      CUDA_TRY(upload(&h->vals, v.data(), size_t(nnz) * 4, &total));
+    } else {
+      CUDA_TRY(upload(&h->vals, values, size_t(nnz) * 8, &total));
+    }
+    CUSPARSE_TRY(cusparseCreate(&h->handle));
+    const cudaDataType dt = tau == 4 ? CUDA_R_32F : CUDA_R_64F;
+    CUSPARSE_TRY(cusparseCreateCsr(&h->mat, n_rows, n_cols, nnz, h->row_ptr, h->col_idx, h->vals,
+                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I,
+                                   CUSPARSE_INDEX_BASE_ZERO, dt));
+    *out = h.release();
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_csr_spmv(ehyb_csr* h, const void* x_dev, void* y_dev, int alg, void* stream) {
+  EHYB_TRY {
+    if (!h) return fail("null handle");
+    DeviceGuard guard(h->device);
+    const cudaDataType dt = h->tau == 4 ? CUDA_R_32F : CUDA_R_64F;
+    cusparseDnVecDescr_t vx, vy;
+    CUSPARSE_TRY(cusparseCreateDnVec(&vx, h->n_cols, const_cast<void*>(x_dev), dt));
+    CUSPARSE_TRY(cusparseCreateDnVec(&vy, h->n_rows, y_dev, dt));
+    CUSPARSE_TRY(cusparseSetStream(h->handle, static_cast<cudaStream_t>(stream)));
+    const cusparseSpMVAlg_t a = alg == 2 ? CUSPARSE_SPMV_CSR_ALG2 : CUSPARSE_SPMV_CSR_ALG1;
+    double one_d = 1.0, zero_d = 0.0;
+    float one_f = 1.0f, zero_f = 0.0f;
+    const void* alpha = h->tau == 4 ? static_cast<const void*>(&one_f) : &one_d;
+    const void* beta = h->tau == 4 ? static_cast<const void*>(&zero_f) : &zero_d;
+    size_t need = 0;
+    CUSPARSE_TRY(cusparseSpMV_bufferSize(h->handle, CUSPARSE_OPERATION_NON_TRANSPOSE, alpha, h->mat,
+                                         vx, beta, vy, dt, a, &need));
+    if (need > h->buffer_bytes) {
+      if (h->buffer) cudaFree(h->buffer);
+      h->buffer = nullptr;
+      CUDA_TRY(cudaMalloc(&h->buffer, need));
+      h->buffer_bytes = need;
+    }
+    CUSPARSE_TRY(cusparseSpMV(h->handle, CUSPARSE_OPERATION_NON_TRANSPOSE, alpha, h->mat, vx, beta,
+                              vy, dt, a, h->buffer));
+    cusparseDestroyDnVec(vx);
+    cusparseDestroyDnVec(vy);
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_csr_destroy(ehyb_csr* h) {
+  if (!h) return 0;
+  DeviceGuard guard(h->device);
+  delete h;
+  return 0;
+}
+
+}  // extern "C"
