@@ -1,0 +1,394 @@
+#!/usr/bin/env python3
+"""EHYB SpMV benchmark (BASELINE.json metric: SpMV GFLOP/s = 2*nnz/t and
+achieved HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+    python bench.py --impl reference ...      # the reference CPU engine arm
+
+One step = one EHYB SpMV y = A x over the whole matrix (one fused kernel
+launch). N=1 workload: BASELINE configs[1] (cfg2: 27-point 128^3 stencil,
+random symmetric permutation, fp64). Prints ONE JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMV GFLOP/s (2*nnz/t) and achieved HBM GB/s vs peak"
+UNIT = "GFLOP/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_workload(name: str):
+    """Matrix + native preprocessing (timed like cli.py:199-219)."""
+    import paper_2204_06666_b200 as E
+    from paper_2204_06666_b200 import workloads as W
+
+    t0 = time.perf_counter()
+    n, r, c, v, tau = W.build_config(name)
+    t_gen = time.perf_counter() - t0
+    m = E.CooMatrix(n, n, r, c, v)
+    del r, c, v
+    params = E.compute_params(n, tau, E.B200_PROFILE)
+    t0 = time.perf_counter()
+    g = E.build_graph(m)
+    parts = E.partition_graph(g, params.n_parts, params.vec_cache_size, seed=0)
+    t1 = time.perf_counter()
+    cls = E.classify_rows(m, parts)
+    plan = E.build_reorder_plan(cls, params, parts)
+    e = E.assemble_ehyb(m, plan, params, parts)
+    t2 = time.perf_counter()
+    del g, cls
+    return m, e, dict(generate_s=t_gen, partition_s=t1 - t0, reorder_assemble_s=t2 - t1)
+
+
+def golden_y_digest(name: str):
+    path = os.path.join(ROOT, "tests", "golden", f"config_{name}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh)
+
+
+def cpu_engine_sample(e, xr, budget_s: float, threads: int):
+    """Time the C restatement of the reference engine (oracle/) on a bounded
+    sample: whole product if it fits the budget, else the first partitions /
+    ER slices. Returns (gflops, seconds per sample, flops per sample, desc)."""
+    from oracle import c_oracle
+
+    prep = c_oracle.Prepared(e)
+    y = np.empty(e.padded_dimension, prep.dt)
+    t0 = time.perf_counter()
+    prep.spmv(xr, threads, out=y)
+    t_full = time.perf_counter() - t0
+    nnz_full = e.nnz
+    if t_full <= budget_s:
+        parts, er = (0, e.n_parts), (0, prep.n_er_slices)
+        flops = 2 * nnz_full
+        desc = "full product"
+    else:
+        frac = max(budget_s / t_full, 1.0 / e.n_parts)
+        p_hi = max(1, int(e.n_parts * frac))
+        s_hi = int(prep.n_er_slices * frac)
+        parts, er = (0, p_hi), (0, s_hi)
+        vec = e.params.vec_cache_size
+        nnz_ell = int(e.ell_row_widths[: p_hi * vec].sum())
+        nnz_er = int(e.er_row_widths[: s_hi * e.params.warp_size].sum())
+        flops = 2 * (nnz_ell + nnz_er)
+        desc = f"partitions [0,{p_hi}) of {e.n_parts} + ER slices [0,{s_hi}) of {prep.n_er_slices}"
+    return prep, parts, er, y, flops, desc
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU SpMV path (engine.py:108-216),
+    restated in C (oracle/ehyb_oracle.c), all host threads, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import paper_2204_06666_b200 as E
+    from paper_2204_06666_b200 import workloads as W
+    from golden_util import digest
+
+    m, e, prep_t = build_workload(args.config)
+    gold = golden_y_digest(args.config)
+    if gold is not None and digest(e.val_ell) != gold["digests"]["val_ell"]:
+        raise SystemExit("reference arm: EHYB arrays differ from the reference's digests")
+    x = W.deterministic_vector(e.dimension, 0)
+    xr = E.permute_vector(x, e.plan)
+    threads = len(os.sched_getaffinity(0))
+    per_step_budget = max(0.05, 120.0 / max(1, args.steps + args.warmup))
+    prep, parts, er, y, flops, desc = cpu_engine_sample(e, xr, per_step_budget, threads)
+    for _ in range(args.warmup):
+        prep.spmv(xr, threads, out=y, parts=parts, er_slices=er)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prep.spmv(xr, threads, out=y, parts=parts, er_slices=er)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = flops / dt / 1e9
+    desc_full = f"{desc} per step ({flops} flops), C restatement of engine.py spmv_ehyb"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if e.params.tau == 8 else "f32",
+        "data": "synthetic", "config": config_block(args, m, e),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": desc_full},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "preprocessing_s": prep_t,
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def config_block(args, m, e):
+    from paper_2204_06666_b200 import workloads as W
+
+    return {
+        "workload": f"{args.config}: {W.CONFIGS[args.config][0]}",
+        "n": int(e.dimension), "nnz": int(m.nnz), "tau": int(e.params.tau),
+        "profile": "DeviceProfile(148, 32, 231424) (B200_PROFILE)",
+        "n_parts": int(e.n_parts), "vec_cache_size": int(e.params.vec_cache_size),
+        "nnz_ell": int(e.nnz_ell), "nnz_er": int(e.nnz_er),
+        "l2_policy": "inputs larger than L2 (matrix stream per step >> 126 MB L2)",
+        "parallelism": f"one CTA per partition x{e.n_parts}",
+    }
+
+
+def run_gpu(args):
+    import torch
+
+    import paper_2204_06666_b200 as E
+    from paper_2204_06666_b200 import workloads as W
+    from golden_util import digest
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2204_06666_b200 import distributed as D
+
+        return D.bench_main(args)
+
+    dev = 0
+    torch.cuda.set_device(dev)
+    m, e, prep_t = build_workload(args.config)
+    nnz = m.nnz
+    flops = 2 * nnz
+    bmin = E.min_bytes(e)
+    gold = golden_y_digest(args.config)
+
+    dm = E.device_matrix(e, dev)
+    info = dm.info()
+    stream = torch.cuda.Stream(dev)
+    x = W.deterministic_vector(e.dimension, 0)
+    xr_host = E.permute_vector(x, e.plan)
+    dt_t = dm.torch_dtype
+    with torch.cuda.stream(stream):
+        xr = torch.from_numpy(xr_host).to(f"cuda:{dev}", dt_t)
+        y = torch.empty_like(xr)
+    stream.synchronize()
+
+    # correctness gate: bitwise against the reference's own y (golden digest)
+    dm.spmv(xr, y, fma=args.fma, stream=stream)
+    stream.synchronize()
+    parity = "unchecked"
+    if gold is not None and not args.fma:
+        ok = digest(y.cpu().numpy()) == gold["y_reordered"]
+        parity = "bitwise == reference y (sha256)" if ok else "MISMATCH"
+        if not ok:
+            log("WARNING: GPU y differs from the reference digest")
+
+    # ---- device-resident timed region (value)
+    for _ in range(args.warmup):
+        dm.spmv(xr, y, fma=args.fma, stream=stream)
+    stream.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            dm.spmv(xr, y, fma=args.fma, stream=stream)
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+    t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    value = flops / t_step / 1e9
+    achieved = bmin / t_step / 1e9
+    peak, peak_src = measured_peak()
+
+    # ---- cuSPARSE CSR comparator, same protocol
+    cus = {}
+    if not args.no_cusparse:
+        csr = E.coo_to_csr(m)
+        from paper_2204_06666_b200.device import DeviceCsr
+
+        dcsr = DeviceCsr(csr.n_rows, csr.n_cols, csr.row_ptr, csr.col_idx, csr.values,
+                         tau=e.params.tau, device=dev)
+        xu = torch.from_numpy(x).to(f"cuda:{dev}", dt_t)
+        yu = torch.empty_like(xu)
+        for alg in (1, 2):
+            for _ in range(max(3, args.warmup)):
+                dcsr.spmv(xu, yu, alg, stream)
+            stream.synchronize()
+            k = max(10, min(args.steps, 200))
+            ev0.record(stream)
+            for _ in range(k):
+                dcsr.spmv(xu, yu, alg, stream)
+            ev1.record(stream)
+            ev1.synchronize()
+            t = ev0.elapsed_time(ev1) / 1e3 / k
+            cus[f"csr_alg{alg}_gflops"] = flops / t / 1e9
+            cus[f"csr_alg{alg}_ms"] = t * 1e3
+        cus["ehyb_speedup_vs_best"] = value / max(cus["csr_alg1_gflops"], cus["csr_alg2_gflops"])
+        del dcsr, xu, yu, csr
+
+    # ---- end-to-end through the public API with pinned host buffers
+    x_pin = torch.from_numpy(x.astype(dm.dtype)).pin_memory().numpy()
+    y_pin = torch.empty(e.dimension, dtype=dt_t).pin_memory().numpy()
+    for _ in range(max(3, min(args.warmup, 10))):
+        dm.spmv_host(x_pin, user_order=True, fma=args.fma, out=y_pin)
+    k_e2e = max(5, min(args.steps, 100))
+    t0 = time.perf_counter()
+    for _ in range(k_e2e):
+        dm.spmv_host(x_pin, user_order=True, fma=args.fma, out=y_pin)
+    t_e2e = (time.perf_counter() - t0) / k_e2e
+    tb = e.params.tau
+
+    # ---- CPU baseline: C restatement of the reference engine, host cores
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        prep, parts, er, yc, cflops, desc = cpu_engine_sample(e, xr_host, 2.0, threads)
+        reps = []
+        t_end = time.perf_counter() + args.cpu_seconds
+        while time.perf_counter() < t_end or len(reps) < 3:
+            t0 = time.perf_counter()
+            prep.spmv(xr_host, threads, out=yc, parts=parts, er_slices=er)
+            reps.append(time.perf_counter() - t0)
+        tc = statistics.median(reps)
+        cpu = {"value": cflops / tc / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{desc}, median of {len(reps)} reps (oracle/ehyb_oracle.c, "
+                         f"C restatement of engine.py spmv_ehyb, OpenMP)"}
+
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as fh:
+            traffic = json.load(fh).get(args.config, {}).get("dram_bytes_per_launch")
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if tb == 8 else "f32",
+        "data": "synthetic", "config": config_block(args, m, e),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bmin,
+                     "model": "nnz_ell*(tau+2) + nnz_er*(tau+4) + 2*n*tau (SURVEY.md 8d)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": flops / t_e2e / 1e9, "unit": UNIT,
+                "h2d_bytes_per_step": int(e.dimension * tb),
+                "d2h_bytes_per_step": int(e.dimension * tb),
+                "ms_per_step": t_e2e * 1e3,
+                "api": "DeviceMatrix.spmv_host(x, user_order=True): pinned H2D, permute, "
+                       "fused SpMV, unpermute, D2H, sync"},
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+        "parity": parity,
+        "cusparse": cus,
+        "kernel": {"avg_us": t_step * 1e6, "effective_gbs": achieved,
+                   "traffic_model_bytes": E.traffic_model(e), "device_info": info},
+        "preprocessing": dict(prep_t, prep_to_spmv_ratio=(prep_t["partition_s"]
+                                                          + prep_t["reorder_assemble_s"]) / t_step),
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--fma", action="store_true", help="fused multiply-add mode")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

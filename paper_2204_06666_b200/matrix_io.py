@@ -111,3 +111,133 @@ def coo_to_csr(m: CooMatrix) -> CsrMatrix:
 def csr_to_coo(m: CsrMatrix) -> CooMatrix:
     rows = np.repeat(np.arange(m.n_rows, dtype=np.int64), np.diff(m.row_ptr))
     return CooMatrix(m.n_rows, m.n_cols, rows, m.col_idx.copy(), m.values.copy())
+
+
+# --------------------------------------------------------------------------
+# .ehyb container (reference matrix_io.py:276-474): persists an assembled
+# EhybMatrix so preprocessing is paid once (SPEC.md amortisation argument).
+#   "EHYB" | version u32 | tau u32 | payload | crc32(payload) u32, little-endian;
+#   payload = every field as (u64 byte length, bytes): 7 u64 scalars, then
+#   the tables as i32 and the bodies as u16 / u32 / f32|f64.
+# --------------------------------------------------------------------------
+
+import struct as _struct
+import zlib as _zlib
+
+_MAGIC = b"EHYB"
+_VERSION = 1
+_SCALARS = ("dimension", "padded_dimension", "k", "n_parts", "vec_cache_size", "warp_size",
+            "n_er_rows")
+# (field, dtype) in payload order; "val" resolves to f32 / f64 by tau
+_ARRAYS = (("reorder_table", "<i4"), ("inverse_table", "<i4"), ("arrange_table", "<i4"),
+           ("y_idx_er", "<i4"), ("part_boundary", "<i4"), ("position_ell", "<i4"),
+           ("width_ell", "<i4"), ("ell_row_widths", "<i4"), ("col_ell", "<u2"),
+           ("val_ell", "val"), ("position_er", "<i4"), ("width_er", "<i4"),
+           ("er_row_widths", "<i4"), ("col_er", "<u4"), ("val_er", "val"))
+
+
+def _field_source(e, name):
+    if name in ("reorder_table", "inverse_table", "arrange_table", "y_idx_er"):
+        return getattr(e.plan, name)
+    return getattr(e, name)
+
+
+def write_ehyb_container(e, sink) -> None:
+    """Serialise an EhybMatrix; read_ehyb_container inverts it bit-exactly."""
+    tau = e.params.tau
+    vdt = "<f4" if tau == 4 else "<f8"
+    scal = dict(dimension=e.dimension, padded_dimension=e.padded_dimension, k=e.params.k,
+                n_parts=e.params.n_parts, vec_cache_size=e.params.vec_cache_size,
+                warp_size=e.params.warp_size, n_er_rows=e.plan.n_er_rows)
+    chunks = []
+    for name in _SCALARS:
+        chunks.append(_struct.pack("<QQ", 8, int(scal[name])))
+    for name, dt in _ARRAYS:
+        raw = np.ascontiguousarray(_field_source(e, name), vdt if dt == "val" else dt).tobytes()
+        chunks.append(_struct.pack("<Q", len(raw)))
+        chunks.append(raw)
+    payload = b"".join(chunks)
+    blob = (_MAGIC + _struct.pack("<II", _VERSION, tau) + payload
+            + _struct.pack("<I", _zlib.crc32(payload) & 0xFFFFFFFF))
+    if isinstance(sink, (str, bytes)) or hasattr(sink, "__fspath__"):
+        with open(sink, "wb") as fh:
+            fh.write(blob)
+    else:
+        sink.write(blob)
+
+
+def read_ehyb_container(source):
+    """Deserialise a .ehyb container (CRC checked before any field is read);
+    raises ContainerError on bad magic / version / tag, truncation, CRC or
+    inconsistent contents."""
+    from .format import EhybMatrix, EhybParams, ReorderPlan
+
+    if isinstance(source, (bytes, bytearray)):
+        blob = bytes(source)
+    elif isinstance(source, str) or hasattr(source, "__fspath__"):
+        with open(source, "rb") as fh:
+            blob = fh.read()
+    else:
+        blob = source.read()
+    if len(blob) < 16:
+        raise ContainerError("truncated stream: missing header")
+    if blob[:4] != _MAGIC:
+        raise ContainerError("bad magic: not an EHYB container")
+    version, tau = _struct.unpack_from("<II", blob, 4)
+    if version != _VERSION:
+        raise ContainerError(f"unsupported container version {version}")
+    if tau not in (4, 8):
+        raise ContainerError(f"invalid precision tag {tau}")
+    view = memoryview(blob)[12:-4]
+    (crc,) = _struct.unpack_from("<I", blob, len(blob) - 4)
+    if (_zlib.crc32(view) & 0xFFFFFFFF) != crc:
+        raise ContainerError("checksum failure: payload does not match CRC32")
+    off = 0
+
+    def take(what):
+        nonlocal off
+        if off + 8 > len(view):
+            raise ContainerError(f"truncated stream while reading {what} length")
+        (ln,) = _struct.unpack_from("<Q", view, off)
+        off += 8
+        if off + ln > len(view):
+            raise ContainerError(f"truncated stream while reading {what}")
+        out = view[off: off + ln]
+        off += ln
+        return out
+
+    sc = {}
+    for name in _SCALARS:
+        raw = take(name)
+        if len(raw) != 8:
+            raise ContainerError(f"bad scalar length for {name}")
+        (sc[name],) = _struct.unpack("<Q", raw)
+    arrs = {}
+    vdt = np.dtype("<f4" if tau == 4 else "<f8")
+    for name, dt in _ARRAYS:
+        d = vdt if dt == "val" else np.dtype(dt)
+        raw = take(name)
+        if len(raw) % d.itemsize:
+            raise ContainerError(f"array length not a multiple of item size for {name}")
+        arrs[name] = np.frombuffer(raw, dtype=d).copy()
+    if off != len(view):
+        raise ContainerError("trailing bytes after last field")
+    try:
+        params = EhybParams(k=int(sc["k"]), n_parts=int(sc["n_parts"]),
+                            vec_cache_size=int(sc["vec_cache_size"]), tau=int(tau),
+                            warp_size=int(sc["warp_size"]))
+        plan = ReorderPlan(reorder_table=arrs["reorder_table"],
+                           inverse_table=arrs["inverse_table"],
+                           arrange_table=arrs["arrange_table"], y_idx_er=arrs["y_idx_er"],
+                           n_er_rows=int(sc["n_er_rows"]), dimension=int(sc["dimension"]),
+                           padded_dimension=int(sc["padded_dimension"]))
+        e = EhybMatrix(params=params, plan=plan, dimension=int(sc["dimension"]),
+                       padded_dimension=int(sc["padded_dimension"]),
+                       **{k: arrs[k] for k in ("val_ell", "col_ell", "position_ell", "width_ell",
+                                               "part_boundary", "ell_row_widths", "val_er",
+                                               "col_er", "position_er", "width_er",
+                                               "er_row_widths")})
+        e.check()
+    except ValueError as exc:
+        raise ContainerError(f"inconsistent container contents: {exc}") from exc
+    return e

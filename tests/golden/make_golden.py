@@ -9,6 +9,7 @@ writes are committed and travel to the GPU box.
 
     python tests/golden/make_golden.py small            -> small_cases.npz / small_cases.json
     python tests/golden/make_golden.py corpus           -> corpus_digests.json
+    python tests/golden/make_golden.py container        -> container_digests.json
     python tests/golden/make_golden.py config cfg1 ...  -> config_<name>.json
 
 Fixtures hold full arrays for small cases and golden digests (golden_util.digest:
@@ -222,12 +223,32 @@ def cmd_config(ehyb, names):
         del m, g, parts, cls, plan, e, arr, r, c, v, y, yu, csr, ycsr
 
 
+def cmd_container(ehyb):
+    """Digests of the reference's .ehyb container bytes (matrix_io.py:337-377)
+    for every small case."""
+    import hashlib
+    import io
+
+    out = {}
+    for name, (n, r, c, v), tau, prof, assign, nph, reb in small_case_specs():
+        *_, e = run_pipeline(ehyb, n, r, c, v, tau, prof, assignment=assign,
+                             n_parts_hint=nph, rebalance=reb)
+        buf = io.BytesIO()
+        ehyb.write_ehyb_container(e, buf)
+        out[name] = hashlib.sha256(buf.getvalue()).hexdigest()
+    with open(os.path.join(HERE, "container_digests.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print(f"container: {len(out)} digests")
+
+
 def main(argv):
     ehyb = load_reference()
     if argv[0] == "small":
         cmd_small(ehyb)
     elif argv[0] == "corpus":
         cmd_corpus(ehyb)
+    elif argv[0] == "container":
+        cmd_container(ehyb)
     elif argv[0] == "config":
         cmd_config(ehyb, argv[1:])
     else:
