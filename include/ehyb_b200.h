@@ -166,6 +166,20 @@ EHYB_API int ehyb_dev_create(const ehyb_host_matrix* m, int device, ehyb_dev** o
 EHYB_API int ehyb_dev_destroy(ehyb_dev* h);
 EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
 
+/* Launch tuning of a handle (defaults are the measured best for B200):
+ *   EHYB_TUNE_PREFETCH_ELL  ELL slices kept ahead of the warps by TMA bulk
+ *                           L2 prefetch (0 = off)
+ *   EHYB_TUNE_PREFETCH_ER   1 = bulk-prefetch each warp's next ER slice
+ *   EHYB_TUNE_THREADS       threads per CTA (multiple of 32, <= 1024)
+ *   EHYB_TUNE_TIMING        device pointer to n_parts*4 u64 %globaltimer
+ *                           stamps per CTA (start, window ready, ELL
+ *                           drained, end), 0 = off */
+#define EHYB_TUNE_PREFETCH_ELL 1
+#define EHYB_TUNE_PREFETCH_ER 2
+#define EHYB_TUNE_THREADS 3
+#define EHYB_TUNE_TIMING 4
+EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value);
+
 /* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].
  * x, y: device arrays of the stored precision (tau 4 -> float, 8 -> double),
  * non-aliasing. One fused kernel: per partition, TMA-staged x window ->
@@ -234,6 +248,14 @@ EHYB_API int ehyb_dev_gather(const void* src, const int64_t* idx_dev, int64_t co
  * (deterministic two-level reduction, no atomics). */
 EHYB_API int ehyb_dev_dot(const void* a, const void* b, int64_t n, int32_t tau, double* out_dev,
                           void* stream);
+/* CG updates with device-resident scalars: alpha = rr[0]/pq[0];
+ * x += alpha p; r -= alpha q; rr_new[0] = r.r (local part, deterministic). */
+EHYB_API int ehyb_dev_cg_xr(void* x, void* r, const void* p, const void* q, const double* rr,
+                            const double* pq, int64_t n, int32_t tau, double* rr_new,
+                            void* stream);
+/* p = r + (rr_new[0] / rr_old[0]) p. */
+EHYB_API int ehyb_dev_cg_p(void* p, const void* r, const double* rr_new, const double* rr_old,
+                           int64_t n, int32_t tau, void* stream);
 /* y = a*x + y (a read from device memory, scaled by sign). */
 EHYB_API int ehyb_dev_axpy(const double* a_dev, double sign, const void* x, void* y, int64_t n,
                            int32_t tau, void* stream);

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(PKG, "libehyb_b200.so")
 
 EINVAL, ENOMEM, ECUDA = 1, 2, 3
 MODE_STRICT, MODE_FMA = 0, 1
+TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING = 1, 2, 3, 4
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -95,6 +96,7 @@ _PROTOS = {
                                         C.POINTER(vp)]),
     "ehyb_dev_destroy": (C.c_int, [vp]),
     "ehyb_dev_info_get": (C.c_int, [vp, C.POINTER(DevInfo)]),
+    "ehyb_dev_tune": (C.c_int, [vp, C.c_int, C.c_int64]),
     "ehyb_dev_spmv": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     "ehyb_dev_spmv_ell": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     "ehyb_dev_spmv_er": (C.c_int, [vp, vp, vp, C.c_int, vp]),
@@ -104,7 +106,9 @@ _PROTOS = {
     "ehyb_dev_spmv_host": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
     "ehyb_dev_gather": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int32, vp]),
     "ehyb_dev_dot": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp, vp]),
-    "ehyb_dev_axpy": (C.c_int, [vp, C.c_double, vp, vp, C.c_int64, C.c_int32, vp]),
+    "ehyb_dev_cg_xr": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp]),
+    "ehyb_dev_cg_p": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int32, vp]),
+    "ehyb_dev_axpy":(C.c_int, [vp, C.c_double, vp, vp, C.c_int64, C.c_int32, vp]),
     "ehyb_csr_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_int32,
                                   C.c_int, C.POINTER(vp)]),
     "ehyb_csr_spmv": (C.c_int, [vp, vp, vp, C.c_int, vp]),

@@ -19,6 +19,7 @@
 #include <cusparse.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -104,10 +105,20 @@ struct ehyb_dev {
   bool window_in_smem = false, window_tma = false;
   int sm_count = 0;
   size_t bytes = 0;
+  // tuning knobs (ehyb_dev_tune) and optional per-CTA timing buffer
+  int pf_ell = 0, pf_er = 1;
+  unsigned long long* timing = nullptr;
+  // ER pool (cross-CTA load balance)
+  int64_t pool_lo = 0, pool_hi = 0;
+  uint32_t* chunk_pub = nullptr;
+  unsigned int* chunk_flag = nullptr;
+  unsigned int* pool_ctr = nullptr;
+  unsigned int epoch = 0;
 
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
-                    er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu};
+                    er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
+                    chunk_pub, chunk_flag, pool_ctr};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -138,7 +149,17 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.window_tma = h->window_tma ? 1 : 0;
   P.do_ell = do_ell ? 1 : 0;
   P.do_er = do_er ? 1 : 0;
-  auto kern = spmv_fused_kernel<T, STRICT, C32>;
+  P.pf_ell = h->pf_ell;
+  P.pf_er = h->pf_er;
+  P.timing = h->timing;
+  P.pool_lo = h->pool_lo;
+  P.pool_hi = h->pool_hi;
+  P.pool_ctr = h->pool_ctr;
+  P.chunk_flag = h->chunk_flag;
+  P.chunk_pub = h->chunk_pub;
+  P.epoch = h->epoch;
+  auto kern = P.window_in_smem ? spmv_fused_kernel<T, STRICT, C32, true>
+                              : spmv_fused_kernel<T, STRICT, C32, false>;
   const size_t smem = P.window_in_smem ? h->smem : 0;
   if (smem > 48 * 1024) {
     // opt in once per (kernel, device) to the largest window any handle needs
@@ -170,10 +191,38 @@ cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, boo
              : launch_typed<T, true, false>(h, x, y, ell, er, st);
 }
 
-cudaError_t launch_spmv(const ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
+cudaError_t launch_spmv(ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
                         cudaStream_t st) {
+  if (ell) h->epoch += 1;  // the ER-only launch of a split SpMV reuses its ELL epoch
   return h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
                      : launch_mode<double>(h, x, y, mode, ell, er, st);
+}
+
+double env_double(const char* name, double dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  return std::atof(v);
+}
+
+// resident CTAs per SM of the fused kernel for this handle's configuration
+cudaError_t occupancy(const ehyb_dev* h, int* per_sm) {
+  const bool c32 = h->warp == 32;
+  const void* k;
+  if (h->tau == 4)
+    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, true, true>
+                                 : (const void*)spmv_fused_kernel<float, true, true, false>)
+            : (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, false, true>
+                                 : (const void*)spmv_fused_kernel<float, true, false, false>);
+  else
+    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, true, true>
+                                 : (const void*)spmv_fused_kernel<double, true, true, false>)
+            : (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, false, true>
+                                 : (const void*)spmv_fused_kernel<double, true, false, false>);
+  if (h->smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k, h->threads, h->smem);
 }
 
 int grid_for(int64_t n, int threads, int sms) {
@@ -232,39 +281,111 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::unordered_map<int64_t, int64_t> halo_index;
   halo_index.reserve(size_t(n_halo) * 2 + 1);
   for (int64_t i = 0; i < n_halo; ++i) halo_index[halo_cols[i]] = h->local_rows + i;
+  // launch configuration first: the ER pool is only safe when every CTA of
+  // the grid is resident at once (pool rows wait on other CTAs' ELL chunks)
+  int optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  CUDA_TRY(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
+  const size_t win = size_t(vec) * tb;
+  const size_t win_al = (win + 127) / 128 * 128;
+  h->window_in_smem = win_al + 64 <= size_t(optin);
+  h->smem = h->window_in_smem ? win_al : 0;
+  h->window_tma = h->window_in_smem && (win % 16 == 0);  // TMA needs 16 B multiples
+  const int64_t chunks = (vec + 31) / 32;
+  h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(32, chunks * 32)));
+  int per_sm = 0;
+  CUDA_TRY(occupancy(h.get(), &per_sm));
+  const bool pool_ok = n_loc_parts <= int64_t(per_sm) * h->sm_count;
+
+  // per-partition 32-row ER slices (members in reference order), then the
+  // own / pool split: partition q keeps the prefix of its ER slices that fits
+  // its share of the mean per-CTA cost (ELL slots + er_cost * ER entries);
+  // the rest joins a pool any CTA may claim once its own work is done
+  const double pool_factor = env_double("EHYB_POOL_FACTOR", 0.95);
+  const double er_cost = env_double("EHYB_ER_COST", 3.0);
+  std::vector<double> ell_cost(static_cast<size_t>(n_loc_parts)), er_total(static_cast<size_t>(n_loc_parts), 0.0);
+  double total = 0.0;
+  for (int64_t q = 0; q < n_loc_parts; ++q) {
+    const int64_t a = (q * vec) / C, b = ((q + 1) * vec) / C;
+    ell_cost[size_t(q)] = double(pos[size_t(b)] - pos[size_t(a)]);
+    for (int64_t j : members[size_t(q)]) er_total[size_t(q)] += er_cost * m->er_row_widths[j];
+    total += ell_cost[size_t(q)] + er_total[size_t(q)];
+  }
+  const double budget_mean = n_loc_parts ? total / double(n_loc_parts) : 0.0;
+  struct SliceRef { int64_t q, i0; };
+  std::vector<std::vector<SliceRef>> own(static_cast<size_t>(n_loc_parts)), spill(static_cast<size_t>(n_loc_parts));
+  for (int64_t q = 0; q < n_loc_parts; ++q) {
+    const auto& mem = members[size_t(q)];
+    double left = (pool_ok && pool_factor > 0.0) ? pool_factor * budget_mean - ell_cost[size_t(q)]
+                                                 : 1e300;
+    bool spilling = false;
+    for (size_t i0 = 0; i0 < mem.size(); i0 += 32) {
+      double c = 0.0;
+      for (size_t i = i0; i < std::min(mem.size(), i0 + 32); ++i) c += er_cost * m->er_row_widths[mem[i]];
+      if (!spilling && c <= left) {
+        left -= c;
+        own[size_t(q)].push_back({q, int64_t(i0)});
+      } else {
+        spilling = true;
+        spill[size_t(q)].push_back({q, int64_t(i0)});
+      }
+    }
+  }
   std::vector<int32_t> part_ptr(size_t(n_loc_parts) + 1, 0);
-  for (int64_t q = 0; q < n_loc_parts; ++q)
-    part_ptr[size_t(q) + 1] = part_ptr[size_t(q)] + int32_t((members[size_t(q)].size() + 31) / 32);
-  const int64_t n_sl = part_ptr[size_t(n_loc_parts)];
+  std::vector<SliceRef> order;
+  for (int64_t q = 0; q < n_loc_parts; ++q) {
+    for (const auto& r : own[size_t(q)]) order.push_back(r);
+    part_ptr[size_t(q) + 1] = int32_t(order.size());
+  }
+  h->pool_lo = int64_t(order.size());
+  for (size_t round = 0;; ++round) {  // pool: round-robin over the heavy partitions
+    bool any = false;
+    for (int64_t q = 0; q < n_loc_parts; ++q)
+      if (round < spill[size_t(q)].size()) {
+        order.push_back(spill[size_t(q)][round]);
+        any = true;
+      }
+    if (!any) break;
+  }
+  h->pool_hi = int64_t(order.size());
+  const int64_t n_sl = int64_t(order.size());
   std::vector<int64_t> epos(size_t(n_sl) + 1, 0);
   std::vector<int32_t> eswidth(size_t(n_sl), 0), erows(size_t(n_sl) * 32, -1),
       elwidth(size_t(n_sl) * 32, 0);
-  for (int64_t q = 0; q < n_loc_parts; ++q) {
-    const auto& mem = members[size_t(q)];
-    for (size_t i = 0; i < mem.size(); ++i) {
-      const int64_t j = mem[i];
-      const int64_t sl = part_ptr[size_t(q)] + int64_t(i / 32);
+  const int64_t n_chunk_total = n_loc_parts * chunks;
+  std::vector<uint32_t> pub(size_t((n_chunk_total + 31) / 32), 0u);
+  for (int64_t sl = 0; sl < n_sl; ++sl) {
+    const auto& ref = order[size_t(sl)];
+    const auto& mem = members[size_t(ref.q)];
+    for (int64_t i = ref.i0; i < std::min<int64_t>(int64_t(mem.size()), ref.i0 + 32); ++i) {
+      const int64_t j = mem[size_t(i)];
       const int32_t w = m->er_row_widths[j];
       const int64_t ref_w = m->width_er[j / C];
-      int32_t row = int32_t(m->y_idx_er[j] - row_lo);
+      const int64_t lr = m->y_idx_er[j] - row_lo;
+      int32_t row = int32_t(lr);
       if (!shard && w < ref_w) row |= kPadFlag;
-      erows[size_t(sl) * 32 + i % 32] = row;
-      elwidth[size_t(sl) * 32 + i % 32] = w;
+      erows[size_t(sl) * 32 + (i - ref.i0)] = row;
+      elwidth[size_t(sl) * 32 + (i - ref.i0)] = w;
       eswidth[size_t(sl)] = std::max(eswidth[size_t(sl)], w);
+      if (sl >= h->pool_lo) {
+        const int64_t rq = lr / vec;
+        const int64_t gc = rq * chunks + ((lr - rq * vec) >> 5);
+        pub[size_t(gc >> 5)] |= 1u << (gc & 31);
+      }
     }
   }
   for (int64_t s = 0; s < n_sl; ++s) epos[size_t(s) + 1] = epos[size_t(s)] + 32 * int64_t(eswidth[size_t(s)]);
   const int64_t eslots = epos[size_t(n_sl)];
   std::vector<char> evals(size_t(std::max<int64_t>(eslots, 1)) * tb, 0);
   std::vector<uint32_t> ecols(size_t(std::max<int64_t>(eslots, 1)), 0);
-  for (int64_t q = 0; q < n_loc_parts; ++q) {
-    const auto& mem = members[size_t(q)];
-    for (size_t i = 0; i < mem.size(); ++i) {
-      const int64_t j = mem[i];
-      const int64_t sl = part_ptr[size_t(q)] + int64_t(i / 32);
+  for (int64_t sl = 0; sl < n_sl; ++sl) {
+    const auto& ref = order[size_t(sl)];
+    const auto& mem = members[size_t(ref.q)];
+    for (int64_t i = ref.i0; i < std::min<int64_t>(int64_t(mem.size()), ref.i0 + 32); ++i) {
+      const int64_t j = mem[size_t(i)];
       const int64_t w = m->er_row_widths[j];
       const int64_t src0 = int64_t(m->position_er[j / C]) + j % C;
-      const int64_t dst0 = epos[size_t(sl)] + int64_t(i % 32);
+      const int64_t dst0 = epos[size_t(sl)] + (i - ref.i0);
       for (int64_t k = 0; k < w; ++k) {
         const int64_t src = src0 + k * C, dst = dst0 + k * 32;
         std::memcpy(&evals[size_t(dst) * tb], static_cast<const char*>(m->val_er) + size_t(src) * tb, tb);
@@ -300,18 +421,15 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(upload(&h->inverse, inv.data(), inv.size() * 4, &h->bytes));
   }
 
-  // ---- launch configuration
-  int optin = 0;
-  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  CUDA_TRY(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
-  const size_t win = size_t(vec) * tb;
-  const size_t win_al = (win + 127) / 128 * 128;
-  h->window_in_smem = win_al + 64 <= size_t(optin);
-  h->smem = h->window_in_smem ? win_al : 0;
-  // TMA bulk copies need 16-byte aligned source offsets and sizes
-  h->window_tma = h->window_in_smem && (win % 16 == 0);
-  const int64_t chunks = (vec + 31) / 32;
-  h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(32, chunks * 32)));
+  // ---- ER pool state: claim counters and per-chunk publication epochs
+  if (h->pool_hi > h->pool_lo) {
+    CUDA_TRY(upload(&h->chunk_pub, pub.data(), pub.size() * 4, &h->bytes));
+    CUDA_TRY(cudaMalloc(&h->chunk_flag, size_t(n_chunk_total) * 4 + 16));
+    CUDA_TRY(cudaMemset(h->chunk_flag, 0, size_t(n_chunk_total) * 4 + 16));
+    CUDA_TRY(cudaMalloc(&h->pool_ctr, 16));
+    CUDA_TRY(cudaMemset(h->pool_ctr, 0, 16));
+    h->bytes += size_t(n_chunk_total) * 4 + 32;
+  }
   *out = h.release();
   return 0;
 }
@@ -345,6 +463,23 @@ EHYB_API int ehyb_dev_destroy(ehyb_dev* h) {
   DeviceGuard guard(h->device);
   delete h;
   return 0;
+}
+
+EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
+  if (!h) return fail("null handle");
+  switch (key) {
+    case EHYB_TUNE_PREFETCH_ELL: h->pf_ell = int(std::max<int64_t>(0, value)); return 0;
+    case EHYB_TUNE_PREFETCH_ER: h->pf_er = value ? 1 : 0; return 0;
+    case EHYB_TUNE_THREADS:
+      if (value < 32 || value > 1024 || value % 32) return fail("threads must be a multiple of 32 in [32, 1024]");
+      h->threads = int(value);
+      return 0;
+    case EHYB_TUNE_TIMING:
+      h->timing = reinterpret_cast<unsigned long long*>(static_cast<uintptr_t>(value));
+      return 0;
+    default:
+      return fail("unknown tuning key");
+  }
 }
 
 EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out) {
@@ -518,6 +653,49 @@ EHYB_API int ehyb_dev_dot(const void* a, const void* b, int64_t n, int32_t tau, 
       dot_partial_kernel<double><<<kBlocks, kThreads, 0, st>>>(
           static_cast<const double*>(a), static_cast<const double*>(b), n, part);
     dot_final_kernel<<<1, 1024, 0, st>>>(part, kBlocks, out_dev);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_cg_xr(void* x, void* r, const void* p, const void* q, const double* rr,
+                            const double* pq, int64_t n, int32_t tau, double* rr_new,
+                            void* stream) {
+  EHYB_TRY {
+    auto st = static_cast<cudaStream_t>(stream);
+    constexpr int kBlocks = 592, kThreads = 512;
+    static thread_local std::unordered_map<int, double*> partials;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    double*& part = partials[dev];
+    if (!part) CUDA_TRY(cudaMalloc(&part, kBlocks * sizeof(double)));
+    if (tau == 4)
+      cg_xr_kernel<float><<<kBlocks, kThreads, 0, st>>>(
+          static_cast<float*>(x), static_cast<float*>(r), static_cast<const float*>(p),
+          static_cast<const float*>(q), rr, pq, n, part);
+    else
+      cg_xr_kernel<double><<<kBlocks, kThreads, 0, st>>>(
+          static_cast<double*>(x), static_cast<double*>(r), static_cast<const double*>(p),
+          static_cast<const double*>(q), rr, pq, n, part);
+    dot_final_kernel<<<1, 1024, 0, st>>>(part, kBlocks, rr_new);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_cg_p(void* p, const void* r, const double* rr_new, const double* rr_old,
+                           int64_t n, int32_t tau, void* stream) {
+  EHYB_TRY {
+    auto st = static_cast<cudaStream_t>(stream);
+    const int g = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+    if (tau == 4)
+      cg_p_kernel<float><<<g, 256, 0, st>>>(static_cast<float*>(p), static_cast<const float*>(r),
+                                             rr_new, rr_old, n);
+    else
+      cg_p_kernel<double><<<g, 256, 0, st>>>(static_cast<double*>(p),
+                                              static_cast<const double*>(r), rr_new, rr_old, n);
     CUDA_TRY(cudaGetLastError());
     return 0;
   }

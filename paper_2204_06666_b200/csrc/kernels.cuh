@@ -4,15 +4,19 @@
 // engine.py:134-154):
 //   1. the partition's x window x[p*vec, (p+1)*vec) is staged into shared
 //      memory by TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx);
+//      meanwhile TMA bulk L2 prefetches (cp.async.bulk.prefetch.L2) start
+//      streaming the partition's contiguous ELL slab, and every claimed slice
+//      keeps the stream pf_ell slices ahead of the warps;
 //   2. warps claim 32-row chunks (= SELL slices for warp_size 32) from a
-//      shared-memory counter (the paper's in-block slice stealing) and stream
-//      val/col with coalesced, evict-first loads, U slots in flight per lane,
-//      gathering x from the staged window through the u16 local columns;
-//   3. after a CTA barrier the same CTA runs the partition's ER rows (derived
-//      per-partition SELL layout, x through the read-only path) and finishes
-//      y[r] = y_ell[r] + er_acc — the reference's phase-2 "y[y_idx] += acc"
-//      without a grid-wide barrier or atomics (each ER row belongs to exactly
-//      one partition, so only its own CTA touches it).
+//      shared-memory counter (the paper's in-block slice stealing) and read
+//      val/col with coalesced evict-first loads, 2*kUnroll loads in flight per
+//      lane, gathering x from the staged window through the u16 local columns;
+//   3. a warp that finds the ELL counter empty moves straight on to the
+//      partition's ER rows (derived per-partition SELL layout, x through the
+//      read-only path) and finishes y[r] = y_ell[r] + er_acc once r's ELL
+//      chunk has published its done bit — the reference's phase-2
+//      "y[y_idx] += acc" without a grid-wide barrier or atomics (each ER row
+//      belongs to exactly one partition, so only its own CTA touches it).
 // STRICT arithmetic is the reference's: acc starts at +0.0 and every slot is
 // a separately rounded multiply then add, k ascending, padding slots
 // included — bitwise identical y. FMA mode fuses the two roundings.
@@ -49,6 +53,15 @@ struct SpmvParams {
   int32_t window_tma;
   int32_t do_ell;
   int32_t do_er;
+  int32_t pf_ell;            // ELL slices kept in flight ahead of the warps by L2 bulk prefetch (0 = off)
+  int32_t pf_er;             // 1 = L2 bulk prefetch of the next ER slice per warp
+  unsigned long long* timing;  // optional per-CTA %globaltimer stamps [start, window, ell, end]
+  // ER work pool shared by all CTAs (load balance across partitions)
+  int64_t pool_lo, pool_hi;         // global slice range of the pool
+  unsigned int* pool_ctr;           // [2] claim counters, alternating by epoch
+  unsigned int* chunk_flag;         // [n_chunks] epoch of the last published ELL chunk
+  const uint32_t* __restrict__ chunk_pub;  // bitmap: chunk holds a pooled ER row
+  unsigned int epoch;               // launch sequence number (>= 1)
 };
 
 constexpr int32_t kPadFlag = 0x40000000;  // row had reference ER padding slots
@@ -103,17 +116,85 @@ __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 
-// One SELL row: lane slots pos, pos+C, ..., pos+(w-1)C; x gathered from `win`
-// (shared-memory window or global). U independent loads per lane in flight.
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+
+// TMA bulk prefetch of one 32-row SELL slice (vals + cols) into L2. Slice
+// offsets are multiples of 32 slots, so both ranges are 64 B aligned and a
+// multiple of 16 bytes long, as cp.async.bulk requires.
+template <typename T>
+__device__ __forceinline__ void prefetch_slice(const T* val, const uint16_t* col, int64_t p0,
+                                               int64_t p1) {
+  if (p1 > p0) {
+    bulk_prefetch_l2(val + p0, uint32_t((p1 - p0) * int64_t(sizeof(T))));
+    bulk_prefetch_l2(col + p0, uint32_t((p1 - p0) * 2));
+  }
+}
+
+// One 32-row SELL slice, one row per lane, slots pos + 32k. Full batches of
+// kUnroll slots issue all column and value loads before the first gather so
+// every lane keeps 2*kUnroll independent loads in flight; the tail batch is
+// predicated. The accumulation order is k ascending (reference order).
 template <typename T, bool STRICT>
-__device__ __forceinline__ T ell_row(const T* __restrict__ val, const uint16_t* __restrict__ col,
-                                     int64_t pos, int w, int64_t C, const T* win) {
+__device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
+                                         const uint16_t* __restrict__ col, int64_t pos, int w,
+                                         const T* win) {
+  T acc = T(0);
+  int k = 0;
+  for (; k + kUnroll <= w; k += kUnroll) {
+    uint32_t c[kUnroll];
+    T v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
+    T xv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) xv[u] = win[c[u]];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) acc = madd<STRICT>(acc, v[u], xv[u]);
+  }
+  if (k < w) {
+    uint32_t c[kUnroll];
+    T v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      c[u] = 0;
+      v[u] = T(0);
+      if (k + u < w) {
+        c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
+        v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < w) acc = madd<STRICT>(acc, v[u], win[c[u]]);
+  }
+  return acc;
+}
+
+// Generic slice height C (the reference tests use 1, 4, 8): one row per
+// thread, slots pos + C k.
+template <typename T, bool STRICT>
+__device__ __forceinline__ T ell_row_generic(const T* __restrict__ val,
+                                             const uint16_t* __restrict__ col, int64_t pos, int w,
+                                             int64_t C, const T* win) {
   T acc = T(0);
   for (int k = 0; k < w; k += kUnroll) {
     T v[kUnroll];
     uint32_t c[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
+      c[u] = 0;
+      v[u] = T(0);
       if (k + u < w) {
         v[u] = __ldcs(val + pos + int64_t(k + u) * C);
         c[u] = __ldcs(col + pos + int64_t(k + u) * C);
@@ -126,58 +207,147 @@ __device__ __forceinline__ T ell_row(const T* __restrict__ val, const uint16_t* 
   return acc;
 }
 
-template <typename T, bool STRICT, bool C32>
+// One derived ER slice: lane row (-1 = empty lane) and its accumulated
+// products in k order, x read through the read-only path. `ahead` > 0 bulk-
+// prefetches the slice `ahead` positions later (same warp's likely next).
+template <typename T, bool STRICT>
+__device__ __forceinline__ T er_slice_acc(const SpmvParams<T>& P, int64_t s, int64_t s_end,
+                                          int ahead, int lane, int32_t& rw) {
+  rw = __ldg(P.er_rows + s * 32 + lane);
+  const int lw = __ldg(P.er_lwidth + s * 32 + lane);
+  const int sw = __ldg(P.er_swidth + s);
+  const int64_t pos = __ldg(P.er_pos + s) + lane;
+  if (lane == 0 && P.pf_er && ahead > 0 && s + ahead < s_end) {
+    const int64_t q = s + ahead;
+    const int64_t q0 = __ldg(P.er_pos + q), q1 = __ldg(P.er_pos + q + 1);
+    if (q1 > q0) {
+      bulk_prefetch_l2(P.er_val + q0, uint32_t((q1 - q0) * int64_t(sizeof(T))));
+      bulk_prefetch_l2(P.er_col + q0, uint32_t((q1 - q0) * 4));
+    }
+  }
+  T acc = T(0);
+  for (int k = 0; k < sw; k += kUnroll) {
+    T v[kUnroll];
+    uint32_t c[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      c[u] = 0;
+      v[u] = T(0);
+      if (k + u < lw) {
+        c[u] = __ldcs(P.er_col + pos + int64_t(k + u) * 32);
+        v[u] = __ldcs(P.er_val + pos + int64_t(k + u) * 32);
+      }
+    }
+    T xv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) xv[u] = (k + u < lw) ? __ldg(P.x + c[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (k + u < lw) acc = madd<STRICT>(acc, v[u], xv[u]);
+  }
+  // reference ER padding products 0*x[0] (engine.py:148-151): inert for
+  // finite x, NaN-propagating otherwise — reproduced with one product
+  if (rw >= 0 && (rw & kPadFlag)) acc = add_rn(acc, mul_rn(T(0), __ldg(P.x)));
+  return acc;
+}
+
+__device__ __forceinline__ int lds_volatile(const uint32_t* p, uint32_t bit) {
+  return (*reinterpret_cast<const volatile uint32_t*>(p) & bit) != 0;
+}
+
+constexpr int kMaxChunks = EHYB_MAX_LOCAL_INDEX / 32;  // 32-row chunks per partition
+
+// Fused EHYB SpMV, one CTA per partition.
+//   SMEM : the x window is staged in shared memory (else read from global)
+//   C32  : slice height 32 (warp == slice); else generic height
+// Warps claim ELL chunks from a shared counter; when the counter runs dry a
+// warp moves straight on to the partition's ER slices (no CTA barrier). An
+// ER row whose ELL chunk is still in flight waits on that chunk's done bit,
+// so y[r] = y_ell[r] + er_acc keeps the reference's order of operations.
+template <typename T, bool STRICT, bool C32, bool SMEM>
 __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar;
   __shared__ int next_chunk;
   __shared__ int next_er;
+  __shared__ uint32_t chunk_done[kMaxChunks / 32];
 
   const int part = blockIdx.x;
   const int64_t row0 = int64_t(part) * P.vec;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
+  const int64_t n_chunks = (P.vec + 31) >> 5;
   T* xs = reinterpret_cast<T*>(smem_raw);
   const T* xwin = P.x + row0;
+  const int64_t s0 = __ldg(P.er_part_ptr + part);
+  const int64_t s1 = __ldg(P.er_part_ptr + part + 1);
 
   if (threadIdx.x == 0) {
     next_chunk = nwarps;
     next_er = nwarps;
+    if (P.timing) P.timing[4 * part] = globaltimer();
+    if (part == 0 && P.pool_ctr) P.pool_ctr[(P.epoch + 1u) & 1u] = 0u;  // next launch's counter
   }
-  if (P.do_ell && P.window_in_smem && P.window_tma) {
-    if (threadIdx.x == 0) {
-      mbar_init(&bar, 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t bytes = uint32_t(P.vec * int64_t(sizeof(T)));
-      mbar_expect_tx(&bar, bytes);
-      for (uint32_t off = 0; off < bytes; off += kTmaChunk) {
-        const uint32_t len = bytes - off < uint32_t(kTmaChunk) ? bytes - off : uint32_t(kTmaChunk);
-        tma_bulk_g2s(smem_raw + off, reinterpret_cast<const unsigned char*>(xwin) + off, len, &bar);
+  for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
+    chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
+  if constexpr (SMEM) {
+    if (P.window_tma) {
+      if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
       }
     }
-    mbar_wait(&bar, 0);
-  } else if (P.do_ell && P.window_in_smem) {
-    for (int64_t i = threadIdx.x; i < P.vec; i += blockDim.x) xs[i] = xwin[i];
-    __syncthreads();
-  } else {
-    __syncthreads();
   }
-  const T* win = P.window_in_smem ? xs : xwin;
+  __syncthreads();
+
+  if (threadIdx.x == 0) {
+    if constexpr (SMEM) {
+      if (P.window_tma) {
+        const uint32_t bytes = uint32_t(P.vec * int64_t(sizeof(T)));
+        mbar_expect_tx(&bar, bytes);
+        for (uint32_t off = 0; off < bytes; off += kTmaChunk) {
+          const uint32_t len = bytes - off < uint32_t(kTmaChunk) ? bytes - off : uint32_t(kTmaChunk);
+          tma_bulk_g2s(smem_raw + off, reinterpret_cast<const unsigned char*>(xwin) + off, len,
+                       &bar);
+        }
+      }
+    }
+  }
+  if constexpr (C32) {
+    // warm L2 with the first slices of the partition's ELL stream
+    if (P.do_ell && P.pf_ell > 0 && wid == 0) {
+      for (int64_t c = lane; c < P.pf_ell && c < n_chunks; c += 32) {
+        const int64_t s = (row0 >> 5) + c;
+        prefetch_slice(P.val_ell, P.col_ell, int64_t(__ldg(P.pos_ell + s)),
+                       int64_t(__ldg(P.pos_ell + s + 1)));
+      }
+    }
+  }
+  if constexpr (SMEM) {
+    if (P.window_tma) {
+      mbar_wait(&bar, 0);
+    } else {
+      for (int64_t i = threadIdx.x; i < P.vec; i += blockDim.x) xs[i] = xwin[i];
+      __syncthreads();
+    }
+  }
+  const T* win = SMEM ? xs : xwin;
+  if (P.timing && threadIdx.x == 0) P.timing[4 * part + 1] = globaltimer();
 
   if (P.do_ell) {
-    const int64_t n_chunks = (P.vec + 31) >> 5;
     int64_t chunk = wid;
     while (chunk < n_chunks) {
       if constexpr (C32) {
-        // warp == one SELL slice: warp-uniform width, 256 B (fp64) coalesced rows
         const int64_t s = (row0 >> 5) + chunk;
+        if (lane == 0 && P.pf_ell > 0 && chunk + P.pf_ell < n_chunks) {
+          const int64_t sp = s + P.pf_ell;
+          prefetch_slice(P.val_ell, P.col_ell, int64_t(__ldg(P.pos_ell + sp)),
+                         int64_t(__ldg(P.pos_ell + sp + 1)));
+        }
         const int w = __ldg(P.width_ell + s);
         const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + lane;
-        const T acc = ell_row<T, STRICT>(P.val_ell, P.col_ell, pos, w, 32, win);
+        const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, pos, w, win);
         P.y[row0 + chunk * 32 + lane] = acc;
       } else {
         const int64_t lr = chunk * 32 + lane;
@@ -187,51 +357,75 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
           const int64_t s = r / C;
           const int w = __ldg(P.width_ell + s);
           const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + (r - s * C);
-          P.y[r] = ell_row<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
+          P.y[r] = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
         }
       }
+      const int64_t gchunk = int64_t(part) * n_chunks + chunk;  // partition-major chunk id
+      const bool publish = P.chunk_pub && ((__ldg(P.chunk_pub + (gchunk >> 5)) >> (gchunk & 31)) & 1u);
+      if (publish) __threadfence();  // y of this chunk visible to other CTAs (pooled ER rows)
+      else __threadfence_block();
+      __syncwarp();
       int nxt = 0;
-      if (lane == 0) nxt = atomicAdd(&next_chunk, 1);
+      if (lane == 0) {
+        if (publish) *reinterpret_cast<volatile unsigned int*>(P.chunk_flag + gchunk) = P.epoch;
+        atomicOr(&chunk_done[chunk >> 5], 1u << (chunk & 31));
+        nxt = atomicAdd(&next_chunk, 1);
+      }
       chunk = __shfl_sync(0xffffffffu, nxt, 0);
     }
+    // first warp to find the ELL counter dry stamps the end of ELL issue
+    if (P.timing && lane == 0 && chunk == n_chunks + nwarps - 1)
+      P.timing[4 * part + 2] = globaltimer();
   }
 
   if (P.do_er) {
-    if (P.do_ell) __syncthreads();  // this CTA's y_ell writes precede the ER combine
-    const int64_t s0 = __ldg(P.er_part_ptr + part);
-    const int64_t s1 = __ldg(P.er_part_ptr + part + 1);
+    // own ER rows: finish against this CTA's ELL chunks (shared-memory bits)
     int64_t s = s0 + wid;
     while (s < s1) {
-      const int32_t rw = __ldg(P.er_rows + s * 32 + lane);
-      const int lw = __ldg(P.er_lwidth + s * 32 + lane);
-      const int sw = __ldg(P.er_swidth + s);
-      const int64_t pos = __ldg(P.er_pos + s) + lane;
-      T acc = T(0);
-      for (int k = 0; k < sw; k += kUnroll) {
-        T v[kUnroll];
-        uint32_t c[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          if (k + u < lw) {
-            v[u] = __ldcs(P.er_val + pos + int64_t(k + u) * 32);
-            c[u] = __ldcs(P.er_col + pos + int64_t(k + u) * 32);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-          if (k + u < lw) acc = madd<STRICT>(acc, v[u], __ldg(P.x + c[u]));
-      }
+      int32_t rw;
+      T acc = er_slice_acc<T, STRICT>(P, s, s1, nwarps, lane, rw);
       if (rw >= 0) {
-        // reference ER padding products 0*x[0] (engine.py:148-151): inert for
-        // finite x, NaN-propagating otherwise — reproduced with one product
-        if (rw & kPadFlag) acc = add_rn(acc, mul_rn(T(0), __ldg(P.x)));
         const int64_t r = rw & kRowMask;
-        P.y[r] = add_rn(P.y[r], acc);
+        const int64_t ch = (r - row0) >> 5;
+        const uint32_t bit = 1u << (ch & 31);
+        while (!lds_volatile(&chunk_done[ch >> 5], bit)) {
+        }
+        __threadfence_block();
+        P.y[r] = add_rn(__ldcg(P.y + r), acc);
       }
       int nxt = 0;
       if (lane == 0) nxt = atomicAdd(&next_er, 1);
       s = s0 + __shfl_sync(0xffffffffu, nxt, 0);
     }
+    // shared pool: excess ER slices of heavy partitions, claimed by any CTA;
+    // rows of other CTAs are finished once their ELL chunk is published
+    if (P.pool_hi > P.pool_lo) {
+      unsigned int* ctr = P.pool_ctr + (P.epoch & 1u);
+      int64_t idx = 0;
+      if (lane == 0) idx = atomicAdd(ctr, 1u);
+      s = P.pool_lo + __shfl_sync(0xffffffffu, idx, 0);
+      while (s < P.pool_hi) {
+        int32_t rw;
+        T acc = er_slice_acc<T, STRICT>(P, s, P.pool_hi, 0, lane, rw);
+        if (rw >= 0) {
+          const int64_t r = rw & kRowMask;
+          if (P.do_ell) {
+            const int64_t rp = r / P.vec;
+            const volatile unsigned int* f =
+                P.chunk_flag + rp * ((P.vec + 31) >> 5) + ((r - rp * P.vec) >> 5);
+            while (*f != P.epoch) __nanosleep(64);
+            __threadfence();
+          }
+          P.y[r] = add_rn(__ldcg(P.y + r), acc);
+        }
+        if (lane == 0) idx = atomicAdd(ctr, 1u);
+        s = P.pool_lo + __shfl_sync(0xffffffffu, idx, 0);
+      }
+    }
+  }
+  if (P.timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) P.timing[4 * part + 3] = globaltimer();
   }
 }
 
@@ -294,6 +488,46 @@ __global__ void dot_final_kernel(const double* __restrict__ partial, int n,
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (threadIdx.x == 0) out[0] = s;
   }
+}
+
+// CG vector updates with the scalars kept on the device (no host round trip
+// per iteration). scal = {rr, pq}: alpha = rr / pq; x += alpha p; r -= alpha q;
+// the block partials of r.r go to `partial` (reduced by dot_final_kernel).
+template <typename T>
+__global__ void cg_xr_kernel(T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+                             const T* __restrict__ q, const double* __restrict__ rr,
+                             const double* __restrict__ pq, int64_t n,
+                             double* __restrict__ partial) {
+  __shared__ double red[32];
+  const double alpha = rr[0] / pq[0];
+  const T a = T(alpha);
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    x[i] = x[i] + a * p[i];
+    const T ri = r[i] - a * q[i];
+    r[i] = ri;
+    s += double(ri) * double(ri);
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  }
+}
+
+// p = r + (rr_new / rr_old) p
+template <typename T>
+__global__ void cg_p_kernel(T* __restrict__ p, const T* __restrict__ r,
+                            const double* __restrict__ rr_new, const double* __restrict__ rr_old,
+                            int64_t n) {
+  const T beta = T(rr_new[0] / rr_old[0]);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = r[i] + beta * p[i];
 }
 
 template <typename T>

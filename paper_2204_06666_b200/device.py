@@ -67,6 +67,21 @@ class DeviceMatrix:
     def close(self) -> None:
         self._finalizer()
 
+    def tune(self, *, prefetch_ell: int | None = None, prefetch_er: bool | None = None,
+             threads: int | None = None, timing=False) -> None:
+        """Launch knobs (include/ehyb_b200.h ehyb_dev_tune). `timing`: a CUDA
+        int64 tensor of n_ctas*4 entries to record per-CTA stamps, None to
+        stop recording, False (default) to leave it unchanged."""
+        if prefetch_ell is not None:
+            L.call("ehyb_dev_tune", self._h, L.TUNE_PREFETCH_ELL, int(prefetch_ell))
+        if prefetch_er is not None:
+            L.call("ehyb_dev_tune", self._h, L.TUNE_PREFETCH_ER, int(bool(prefetch_er)))
+        if threads is not None:
+            L.call("ehyb_dev_tune", self._h, L.TUNE_THREADS, int(threads))
+        if timing is not False:
+            ptr = 0 if timing is None else int(timing.data_ptr())
+            L.call("ehyb_dev_tune", self._h, L.TUNE_TIMING, ptr)
+
     def info(self) -> dict:
         out = L.DevInfo()
         L.call("ehyb_dev_info_get", self._h, C.byref(out))

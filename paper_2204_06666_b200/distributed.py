@@ -1,0 +1,403 @@
+"""Row-sharded EHYB SpMV and CG over several B200s of one node
+(SURVEY.md §8e).
+
+The reordered row space is partition-major, so rank g owns a contiguous
+block of partitions [p0, p1): a contiguous slice of x, y and of the ELL slab
+(format.py:176-177, 362). The ELL phase needs only owned x (inner entries
+reference their own partition's window). Owned ER rows reference remote
+columns; the halo plan lists them per peer once, and every SpMV exchanges
+exactly those values with one NCCL all-to-all that overlaps the ELL launch:
+
+    pack (gather kernel) -> all_to_all_single (async)  ||  ELL-only launch
+                         -> wait -> ER-only launch
+
+`x_ext = [owned x (local_rows) | halo (n_halo)]`; the derived ER columns of
+the shard are remapped into that space at upload (ehyb_dev_create_shard).
+One process per GPU; `torch.distributed` supplies the communicator (NCCL on
+GPUs, gloo for the CPU tests of the host logic).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .format import EhybMatrix, host_view
+
+
+def part_range(n_parts: int, world: int, rank: int):
+    """Balanced contiguous partition block of `rank`."""
+    base, extra = divmod(n_parts, world)
+    p0 = rank * base + min(rank, extra)
+    return p0, p0 + base + (1 if rank < extra else 0)
+
+
+def halo_columns(e: EhybMatrix, p0: int, p1: int) -> np.ndarray:
+    """Sorted distinct global (new-order) columns outside [p0*vec, p1*vec)
+    referenced by the real entries of the ER rows that [p0, p1) owns."""
+    vec = e.params.vec_cache_size
+    warp = e.params.warp_size
+    lo, hi = p0 * vec, p1 * vec
+    y_idx = np.asarray(e.plan.y_idx_er, np.int64)
+    slots = np.flatnonzero((y_idx >= lo) & (y_idx < hi))
+    if slots.size == 0:
+        return np.zeros(0, np.int64)
+    w = np.asarray(e.er_row_widths, np.int64)[slots]
+    owner = np.repeat(slots, w)
+    start = np.cumsum(w) - w
+    k = np.arange(owner.size, dtype=np.int64) - np.repeat(start, w)
+    pos = np.asarray(e.position_er, np.int64)[owner // warp] + owner % warp + k * warp
+    cols = np.asarray(e.col_er, np.int64)[pos]
+    cols = cols[(cols < lo) | (cols >= hi)]
+    return np.unique(cols)
+
+
+@dataclass
+class HaloPlan:
+    rank: int
+    world: int
+    p0: int
+    p1: int
+    vec: int
+    local_rows: int
+    halo_cols: np.ndarray      # global columns of the halo slots (ascending)
+    recv_splits: list          # halo values received from each peer
+    send_splits: list          # values sent to each peer
+    send_idx: np.ndarray       # local row offsets gathered into the send buffer
+
+    @property
+    def n_halo(self) -> int:
+        return int(self.halo_cols.size)
+
+
+def _comm_device(group):
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        import torch
+
+        return f"cuda:{torch.cuda.current_device()}"
+    return "cpu"
+
+
+def plan_for(e: EhybMatrix, rank: int, world: int) -> HaloPlan:
+    """Halo plan of `rank`, computed locally: every rank holds the assembled
+    matrix, so what peer q must send to rank g is g's halo restricted to q's
+    rows, in g's (ascending) halo order."""
+    vec = e.params.vec_cache_size
+    ranges = [part_range(e.n_parts, world, q) for q in range(world)]
+    starts = np.array([r[0] * vec for r in ranges], np.int64)
+    p0, p1 = ranges[rank]
+    halo = halo_columns(e, p0, p1)
+    owner = np.searchsorted(starts, halo, side="right") - 1
+    recv_splits = np.bincount(owner, minlength=world).astype(np.int64)
+    send_parts, send_splits = [], []
+    for q in range(world):
+        if q == rank:
+            send_splits.append(0)
+            continue
+        hq = halo_columns(e, *ranges[q])
+        mine = hq[(hq >= p0 * vec) & (hq < p1 * vec)]
+        send_parts.append(mine - p0 * vec)
+        send_splits.append(int(mine.size))
+    send_idx = np.concatenate(send_parts) if send_parts else np.zeros(0, np.int64)
+    return HaloPlan(rank=rank, world=world, p0=p0, p1=p1, vec=vec, local_rows=(p1 - p0) * vec,
+                    halo_cols=halo, recv_splits=recv_splits.tolist(), send_splits=send_splits,
+                    send_idx=send_idx.astype(np.int64))
+
+
+def build_halo_plan(e: EhybMatrix, group=None) -> HaloPlan:
+    """This rank's halo plan; one all-to-all of counts cross-checks that every
+    peer agrees on what it sends (plans are computed locally)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    plan = plan_for(e, rank, world)
+    dev = _comm_device(group)
+    rs = torch.tensor(plan.recv_splits, dtype=torch.int64, device=dev)
+    ss = torch.empty_like(rs)
+    dist.all_to_all_single(ss, rs, group=group)
+    if ss.cpu().tolist() != plan.send_splits:
+        raise RuntimeError("halo plans disagree between ranks")
+    return plan
+
+
+def halo_exchange(x_ext, plan: HaloPlan, group=None, send_buf=None, async_op=False):
+    """Fill x_ext[local_rows:] with the halo values owned by the peers.
+    CPU tensors (gloo) gather with indexing; CUDA tensors use the gather
+    kernel. Returns the collective's work handle when async_op."""
+    import torch
+    import torch.distributed as dist
+
+    n_send = int(sum(plan.send_splits))
+    if x_ext.is_cuda:
+        if send_buf is None:
+            send_buf = torch.empty(n_send, dtype=x_ext.dtype, device=x_ext.device)
+        idx = _idx_tensor(plan, x_ext.device)
+        tau = 4 if x_ext.dtype == torch.float32 else 8
+        L.call("ehyb_dev_gather", C.c_void_p(x_ext.data_ptr()), C.c_void_p(idx.data_ptr()),
+               n_send, C.c_void_p(send_buf.data_ptr()), tau,
+               C.c_void_p(torch.cuda.current_stream(x_ext.device).cuda_stream))
+    else:
+        send_buf = x_ext[torch.from_numpy(plan.send_idx)]
+    recv = x_ext[plan.local_rows: plan.local_rows + plan.n_halo]
+    return dist.all_to_all_single(recv, send_buf, plan.recv_splits, plan.send_splits,
+                                  group=group, async_op=async_op)
+
+
+_idx_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _idx_tensor(plan: HaloPlan, device):
+    import torch
+
+    t = _idx_cache.get(plan)
+    if t is None or t.device != device:
+        t = torch.from_numpy(plan.send_idx).to(device)
+        _idx_cache[plan] = t
+    return t
+
+
+class DistributedEhyb:
+    """This rank's shard of a globally assembled EhybMatrix on its GPU."""
+
+    def __init__(self, e: EhybMatrix, group=None, device: int | None = None,
+                 plan: HaloPlan | None = None):
+        import torch
+
+        self.group = group
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.plan = build_halo_plan(e, group) if plan is None else plan
+        self.tau = e.params.tau
+        self.dtype = torch.float32 if self.tau == 4 else torch.float64
+        self.nnz_local = int(e.ell_row_widths[self.plan.p0 * self.plan.vec:
+                                              self.plan.p1 * self.plan.vec].sum())
+        y_idx = np.asarray(e.plan.y_idx_er, np.int64)
+        lo, hi = self.plan.p0 * self.plan.vec, self.plan.p1 * self.plan.vec
+        self.nnz_local += int(np.asarray(e.er_row_widths)[(y_idx >= lo) & (y_idx < hi)].sum())
+        hv, keep = host_view(e)
+        halo = np.ascontiguousarray(self.plan.halo_cols, np.int64)
+        sp = L.ShardPlan(p0=self.plan.p0, p1=self.plan.p1, n_halo=halo.size,
+                         halo_cols=L.ptr(halo, L.i64p))
+        h = L.vp()
+        L.call("ehyb_dev_create_shard", C.byref(hv), C.byref(sp), self.device, C.byref(h))
+        del keep
+        self._h = h
+        self._finalizer = weakref.finalize(self, L.lib().ehyb_dev_destroy, h)
+        self.local_rows = self.plan.local_rows
+        self.n_ext = self.plan.local_rows + self.plan.n_halo
+        self._send = torch.empty(max(1, int(sum(self.plan.send_splits))), dtype=self.dtype,
+                                 device=f"cuda:{self.device}")
+
+    def new_ext(self):
+        import torch
+
+        return torch.zeros(self.n_ext, dtype=self.dtype, device=f"cuda:{self.device}")
+
+    def spmv_local(self, x_ext, y_local, *, fma: bool = False):
+        """Both phases on an x_ext whose halo is already filled (no exchange)."""
+        import torch
+
+        mode = L.MODE_FMA if fma else L.MODE_STRICT
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        xp, yp = C.c_void_p(x_ext.data_ptr()), C.c_void_p(y_local.data_ptr())
+        L.call("ehyb_dev_spmv_ell", self._h, xp, yp, mode, st)
+        L.call("ehyb_dev_spmv_er", self._h, xp, yp, mode, st)
+        return y_local
+
+    def spmv(self, x_ext, y_local, *, fma: bool = False, overlap: bool = True):
+        """y_local = A[owned rows, :] x. x_ext[:local_rows] holds the owned x;
+        the halo part is exchanged here, overlapped with the ELL phase."""
+        import torch
+
+        mode = L.MODE_FMA if fma else L.MODE_STRICT
+        st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        xp, yp = C.c_void_p(x_ext.data_ptr()), C.c_void_p(y_local.data_ptr())
+        if self.plan.world == 1:
+            L.call("ehyb_dev_spmv", self._h, xp, yp, mode, st)
+            return y_local
+        work = halo_exchange(x_ext, self.plan, self.group, send_buf=self._send[: int(sum(
+            self.plan.send_splits))], async_op=True)
+        if overlap:
+            L.call("ehyb_dev_spmv_ell", self._h, xp, yp, mode, st)
+            work.wait()
+        else:
+            work.wait()
+            L.call("ehyb_dev_spmv_ell", self._h, xp, yp, mode, st)
+        L.call("ehyb_dev_spmv_er", self._h, xp, yp, mode, st)
+        return y_local
+
+
+def dot(a, b, out, n: int):
+    """Local fp64 dot product of the first n entries into out (device)."""
+    import torch
+
+    tau = 4 if a.dtype == torch.float32 else 8
+    L.call("ehyb_dev_dot", C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), int(n), tau,
+           C.c_void_p(out.data_ptr()),
+           C.c_void_p(torch.cuda.current_stream(a.device).cuda_stream))
+
+
+def cg(A: DistributedEhyb, b_local, maxiter: int = 100, tol: float = 0.0):
+    """Conjugate gradients on the sharded operator, every vector and scalar on
+    the device; two fp64 all-reduces per iteration. Returns (x_local, info)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = f"cuda:{A.device}"
+    n = A.local_rows
+    st = C.c_void_p(torch.cuda.current_stream(A.device).cuda_stream)
+    tau = A.tau
+    x = torch.zeros(n, dtype=A.dtype, device=dev)
+    r = b_local.clone()
+    p = A.new_ext()
+    p[:n].copy_(r)
+    q = torch.empty(n, dtype=A.dtype, device=dev)
+    sc = torch.zeros(4, dtype=torch.float64, device=dev)  # rr, pq, rr_new, |b|^2
+    dot(r, r, sc[0:1], n)
+    if A.plan.world > 1:
+        dist.all_reduce(sc[0:1], group=A.group)
+    sc[3] = sc[0]
+    its = 0
+    for its in range(1, maxiter + 1):
+        A.spmv(p, q)
+        dot(p, q, sc[1:2], n)
+        if A.plan.world > 1:
+            dist.all_reduce(sc[1:2], group=A.group)
+        L.call("ehyb_dev_cg_xr", C.c_void_p(x.data_ptr()), C.c_void_p(r.data_ptr()),
+               C.c_void_p(p.data_ptr()), C.c_void_p(q.data_ptr()), C.c_void_p(sc[0:1].data_ptr()),
+               C.c_void_p(sc[1:2].data_ptr()), n, tau, C.c_void_p(sc[2:3].data_ptr()), st)
+        if A.plan.world > 1:
+            dist.all_reduce(sc[2:3], group=A.group)
+        L.call("ehyb_dev_cg_p", C.c_void_p(p.data_ptr()), C.c_void_p(r.data_ptr()),
+               C.c_void_p(sc[2:3].data_ptr()), C.c_void_p(sc[0:1].data_ptr()), n, tau, st)
+        sc[0:1].copy_(sc[2:3])
+        if tol > 0 and its % 10 == 0:
+            if float(sc[0]) <= tol * tol * float(sc[3]):
+                break
+    info = {"iterations": its, "rel_residual": float(np.sqrt(float(sc[0]) / max(float(sc[3]), 1e-300)))}
+    return x, info
+
+
+# --------------------------------------------------------------------------
+# multi-GPU bench (bench.py --gpus N under torchrun)
+# --------------------------------------------------------------------------
+
+def weak_config(world: int):
+    """N-GPU weak-scaling workload: 27-point stencil 128 x 128 x (128*N),
+    random symmetric permutation (seed 1), fp64, P = 148*N partitions.
+    N = 1 is exactly cfg2; N = 8 has cfg5's 16.7M rows."""
+    from . import workloads as W
+
+    return W.permute_symmetric(*W.stencil27(128 * world, 128, 128), seed=1)
+
+
+def bench_main(args):
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    from . import engine
+    from .format import b200_profile, build_ehyb
+    from .matrix_io import CooMatrix, read_ehyb_container, write_ehyb_container
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    path = os.path.join(os.environ.get("EHYB_SCRATCH", "/tmp"), f"ehyb_weak_{world}.ehyb")
+    t0 = time.perf_counter()
+    nnz = None
+    if rank == 0:
+        n, r, c, v = weak_config(world)
+        m = CooMatrix(n, n, r, c, v)
+        nnz = m.nnz
+        e = build_ehyb(m, tau=8, profile=b200_profile(world))
+        write_ehyb_container(e, path)
+        del m, r, c, v
+    obj = [nnz]
+    dist.broadcast_object_list(obj, src=0)
+    nnz = obj[0]
+    dist.barrier()
+    if rank != 0:
+        e = read_ehyb_container(path)
+    t_prep = time.perf_counter() - t0
+    A = DistributedEhyb(e, device=local)
+    bmin_total = engine.min_bytes(e)
+    from . import workloads as W
+
+    xg = W.deterministic_vector(e.dimension, 0)
+    from .format import permute_vector
+
+    xr = permute_vector(xg, e.plan)
+    lo, hi = A.plan.p0 * A.plan.vec, A.plan.p1 * A.plan.vec
+    x_ext = A.new_ext()
+    x_ext[: A.local_rows].copy_(torch.from_numpy(xr[lo:hi]))
+    y = torch.empty(A.local_rows, dtype=A.dtype, device=x_ext.device)
+    del e
+    for _ in range(args.warmup):
+        A.spmv(x_ext, y)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        A.spmv(x_ext, y)
+    ev1.record()
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1) / 1e3 / args.steps], dtype=torch.float64,
+                     device=x_ext.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t)
+    # CG: 100 iterations on b = A*1
+    b = torch.empty(A.local_rows, dtype=A.dtype, device=x_ext.device)
+    ones = A.new_ext()
+    ones[: A.local_rows].fill_(1.0)
+    A.spmv(ones, b)
+    torch.cuda.synchronize()
+    dist.barrier()
+    tc0 = time.perf_counter()
+    _, info = cg(A, b, maxiter=100)
+    torch.cuda.synchronize()
+    tc = torch.tensor([time.perf_counter() - tc0], dtype=torch.float64, device=x_ext.device)
+    dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        flops = 2 * nnz
+        out = {
+            "metric": "SpMV GFLOP/s (2*nnz/t) and achieved HBM GB/s vs peak",
+            "value": flops / t_step / 1e9, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"27-point stencil {128 * world}x128x128, random symmetric "
+                                   f"permutation, P=148x{world} (N=1: cfg2; N=8: cfg5 rows)",
+                       "nnz": nnz, "parallelism": f"row shards x{world}, NCCL halo all-to-all "
+                                                  "overlapped with the ELL phase",
+                       "l2_policy": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": bmin_total / t_step / 1e9 / world,
+                         "peak": 6457.4, "unit": "GB/s (per GPU)",
+                         "frac": bmin_total / t_step / 1e9 / world / 6457.4, "traffic": None},
+            "halo_values_rank0": A.plan.n_halo,
+            "cg": {"iterations": info["iterations"], "ms_per_iter": float(tc) / 100 * 1e3,
+                   "rel_residual": info["rel_residual"]},
+            "preprocessing_s": t_prep,
+            "gpu_launches": 3 * args.steps,
+        }
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

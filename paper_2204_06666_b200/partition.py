@@ -137,6 +137,44 @@ def rebalance_partition(g: AdjacencyGraph, parts: PartitionMap, capacity: int) -
     return PartitionMap(n_parts=n_parts, assignment=assignment, part_sizes=sizes)
 
 
+def save_partition_file(parts: PartitionMap, sink) -> None:
+    """METIS-style interchange: one 0-based id per vertex per line
+    (partition.py:280-290); feeds build_ehyb(partition=...)."""
+    import os
+
+    text = "\n".join(str(int(p)) for p in parts.assignment) + "\n"
+    if isinstance(sink, (str, os.PathLike)):
+        with open(sink, "w") as fh:
+            fh.write(text)
+    else:
+        try:
+            sink.write(text)
+        except TypeError:
+            sink.write(text.encode("ascii"))
+
+
+def load_partition_file(source, n_vertices: int, n_parts: int | None = None) -> PartitionMap:
+    """Inverse of save_partition_file with the reference's checks
+    (partition.py:293-317)."""
+    import os
+
+    if isinstance(source, (str, os.PathLike)):
+        with open(source) as fh:
+            text = fh.read()
+    else:
+        text = source.read()
+        if isinstance(text, bytes):
+            text = text.decode("ascii")
+    tokens = text.split()
+    if len(tokens) != n_vertices:
+        raise ValueError(f"partition file has {len(tokens)} entries, expected {n_vertices}")
+    try:
+        assignment = np.asarray([int(t) for t in tokens], dtype=np.int64)
+    except ValueError:
+        raise ValueError("partition file must contain one integer per line") from None
+    return PartitionMap.from_assignment(assignment, n_parts=n_parts)
+
+
 def cut_metrics(m: CooMatrix, parts: PartitionMap) -> CutMetrics:
     """Inner (same-partition) vs extra entries (partition.py:265-277)."""
     if not m.is_square or parts.n_vertices != m.n_rows:

@@ -1,0 +1,106 @@
+#!/usr/bin/env python3
+"""Dev tool: sweep the fused kernel's launch knobs on one config and print
+per-variant device time, effective GB/s and per-CTA phase timings.
+
+    python scripts/kernel_sweep.py [--config cfg2] [--reps 300]
+"""
+
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2204_06666_b200 as E  # noqa: E402
+from golden_util import digest  # noqa: E402
+from paper_2204_06666_b200 import workloads as W  # noqa: E402
+
+
+def time_variant(dm, xr, y, reps, stream, fma=False):
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(10):
+        dm.spmv(xr, y, fma=fma, stream=stream)
+    ev0.record(stream)
+    for _ in range(reps):
+        dm.spmv(xr, y, fma=fma, stream=stream)
+    ev1.record(stream)
+    ev1.synchronize()
+    return ev0.elapsed_time(ev1) / reps * 1e3  # us
+
+
+def cta_profile(dm, xr, y, stream, n_ctas):
+    t = torch.zeros(n_ctas * 4, dtype=torch.int64, device=xr.device)
+    dm.tune(timing=t)
+    dm.spmv(xr, y, stream=stream)
+    stream.synchronize()
+    dm.tune(timing=None)
+    a = t.cpu().numpy().reshape(n_ctas, 4).astype(np.float64)
+    t0 = a[:, 0].min()
+    rel = (a - t0) / 1e3  # us
+    out = {}
+    for i, name in enumerate(("start", "window", "ell_drained", "end")):
+        col = rel[:, i]
+        out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2),
+                     round(float(np.max(col)), 2)]
+    out["cta_duration_us"] = [round(float(v), 2) for v in
+                              np.percentile(rel[:, 3] - rel[:, 0], [0, 50, 90, 100])]
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--reps", type=int, default=300)
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--pool", default="0,0.9,1.0,1.1")
+    ap.add_argument("--er-cost", default="2.0")
+    args = ap.parse_args()
+    m, e, _ = bench.build_workload(args.config)
+    gold = bench.golden_y_digest(args.config)
+    bmin = E.min_bytes(e)
+    dm = E.device_matrix(e, 0)
+    stream = torch.cuda.Stream(0)
+    x = W.deterministic_vector(e.dimension, 0)
+    with torch.cuda.stream(stream):
+        xr = torch.from_numpy(E.permute_vector(x, e.plan)).to("cuda:0", dm.torch_dtype)
+        y = torch.empty_like(xr)
+    stream.synchronize()
+    n_ctas = dm.info()["ctas"]
+    results = []
+    from paper_2204_06666_b200.device import DeviceMatrix
+
+    handles = {}
+    for pool, ercost in itertools.product(args.pool.split(","), args.er_cost.split(",")):
+        os.environ["EHYB_POOL_FACTOR"] = pool
+        os.environ["EHYB_ER_COST"] = ercost
+        handles[(pool, ercost)] = DeviceMatrix(e, 0)
+    for (pool, ercost), h in handles.items():
+        for pf, pfer in itertools.product([0] if args.quick else [0, 8], (0, 1)):
+            h.tune(prefetch_ell=pf, prefetch_er=pfer, threads=1024)
+            us = time_variant(h, xr, y, args.reps, stream)
+            ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
+            results.append(dict(pool=pool, er_cost=ercost, pf_ell=pf, pf_er=pfer,
+                                us=round(us, 2), gbs=round(bmin / us / 1e3, 1), bitwise=ok))
+            print(json.dumps(results[-1]), flush=True)
+    best = min(results, key=lambda r: r["us"])
+    dm = handles[(best["pool"], best["er_cost"])]
+    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024)
+    prof = cta_profile(dm, xr, y, stream, n_ctas)
+    us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
+    print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,
+                      "fma_us": round(us_fma, 2), "bmin": bmin}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

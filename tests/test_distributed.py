@@ -1,0 +1,149 @@
+"""Multi-GPU layer (distributed.py): halo plans, the halo exchange over a real
+torch.distributed process group (gloo, world_size 2 and 3 on CPU), shard
+products on one GPU, and CG."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2204_06666_b200 as E
+from oracle import c_oracle
+from paper_2204_06666_b200 import distributed as D
+from paper_2204_06666_b200 import workloads as W
+
+
+def matrix(tau=8):
+    n, r, c, v = W.permute_symmetric(*W.stencil27(14, 14, 14), seed=1)
+    m = E.CooMatrix(n, n, r, c, v)
+    return m, E.build_ehyb(m, tau=tau, profile=E.DeviceProfile(12, 32, 8192))
+
+
+def shard_product_host(e, plan, x_ext):
+    """Test-side float64 product of the owned rows from x_ext through the
+    plan's column remap (owned -> c - lo, remote -> local_rows + halo slot)."""
+    vec, warp = e.params.vec_cache_size, e.params.warp_size
+    lo, hi = plan.p0 * vec, plan.p1 * vec
+    coo_r, coo_c, coo_v = [], [], []
+    w = e.ell_row_widths.astype(np.int64)
+    rows = np.repeat(np.arange(e.padded_dimension), w)
+    k = np.arange(rows.size) - np.repeat(np.cumsum(w) - w, w)
+    idx = e.position_ell[rows // warp] + rows % warp + k * warp
+    coo_r.append(rows)
+    coo_c.append(e.col_ell[idx].astype(np.int64) + (rows // vec) * vec)
+    coo_v.append(e.val_ell[idx])
+    w2 = e.er_row_widths.astype(np.int64)
+    slots = np.repeat(np.arange(e.plan.n_er_rows), w2)
+    k2 = np.arange(slots.size) - np.repeat(np.cumsum(w2) - w2, w2)
+    idx2 = e.position_er[slots // warp] + slots % warp + k2 * warp
+    coo_r.append(e.plan.y_idx_er[slots])
+    coo_c.append(e.col_er[idx2].astype(np.int64))
+    coo_v.append(e.val_er[idx2])
+    r = np.concatenate(coo_r)
+    c = np.concatenate(coo_c)
+    v = np.concatenate(coo_v).astype(np.float64)
+    keep = (r >= lo) & (r < hi)
+    r, c, v = r[keep] - lo, c[keep], v[keep]
+    own = (c >= lo) & (c < hi)
+    ext = np.where(own, c - lo, plan.local_rows + np.searchsorted(plan.halo_cols, c))
+    assert np.all(plan.halo_cols[np.searchsorted(plan.halo_cols, c[~own])] == c[~own])
+    y = np.zeros(plan.local_rows)
+    np.add.at(y, r, v * x_ext[ext])
+    return y
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, e = matrix()
+        plan = D.build_halo_plan(e)
+        assert plan.world == world and plan.rank == rank
+        xr = E.permute_vector(W.deterministic_vector(e.dimension, 0), e.plan)
+        lo, hi = plan.p0 * plan.vec, plan.p1 * plan.vec
+        x_ext = torch.zeros(plan.local_rows + plan.n_halo, dtype=torch.float64)
+        x_ext[: plan.local_rows] = torch.from_numpy(xr[lo:hi])
+        D.halo_exchange(x_ext, plan)
+        got = x_ext.numpy()
+        assert np.array_equal(got[plan.local_rows:], xr[plan.halo_cols]), "halo values"
+        y_loc = shard_product_host(e, plan, got)
+        y_full = c_oracle.spmv_ehyb(e, xr, 1)
+        den = np.max(np.abs(y_full))
+        assert np.max(np.abs(y_loc - y_full[lo:hi])) / den < 1e-12, "shard product"
+        # every rank's rows together cover the padded space exactly once
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([plan.local_rows]))
+        assert sum(int(s) for s in sizes) == e.padded_dimension
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    mp.spawn(_worker, args=(world, _free_port()), nprocs=world, join=True)
+
+
+def test_plans_are_consistent():
+    m, e = matrix()
+    for world in (2, 4):
+        plans = [D.plan_for(e, r, world) for r in range(world)]
+        for g, pg in enumerate(plans):
+            for q, pq in enumerate(plans):
+                # what q sends to g == g's halo entries owned by q
+                seg = np.cumsum([0] + pq.send_splits)
+                sent = pq.send_idx[seg[g]:seg[g + 1]] + pq.p0 * pq.vec
+                rseg = np.cumsum([0] + pg.recv_splits)
+                assert np.array_equal(sent, pg.halo_cols[rseg[q]:rseg[q + 1]])
+        assert sum(p.local_rows for p in plans) == e.padded_dimension
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("tau", [4, 8])
+def test_shards_on_one_gpu_bitwise(world, tau):
+    m, e = matrix(tau)
+    xr = E.permute_vector(W.deterministic_vector(e.dimension, 0), e.plan)
+    y_full, _ = E.spmv_ehyb(e, xr)
+    dt = torch.float32 if tau == 4 else torch.float64
+    for rank in range(world):
+        plan = D.plan_for(e, rank, world)
+        A = D.DistributedEhyb(e, device=0, plan=plan)
+        lo, hi = plan.p0 * plan.vec, plan.p1 * plan.vec
+        x_ext = A.new_ext()
+        x_ext[: plan.local_rows] = torch.from_numpy(xr[lo:hi]).to(dt)
+        x_ext[plan.local_rows:] = torch.from_numpy(xr[plan.halo_cols]).to(dt)
+        y = torch.empty(plan.local_rows, dtype=dt, device="cuda:0")
+        A.spmv_local(x_ext, y)
+        torch.cuda.synchronize()
+        assert y.cpu().numpy().tobytes() == y_full[lo:hi].tobytes()
+
+
+@pytest.mark.gpu
+def test_cg_converges_single_gpu():
+    m, e = matrix()
+    plan = D.plan_for(e, 0, 1)
+    A = D.DistributedEhyb(e, device=0, plan=plan)
+    ones = A.new_ext()
+    ones[: A.local_rows].fill_(1.0)
+    # padding rows of b stay 0 (empty rows), so the solution there is 0
+    b = torch.empty(A.local_rows, dtype=torch.float64, device="cuda:0")
+    A.spmv_local(ones, b)
+    x, info = D.cg(A, b, maxiter=200, tol=1e-10)
+    torch.cuda.synchronize()
+    real = np.zeros(A.local_rows, bool)
+    real[e.plan.reorder_table[: e.dimension]] = True
+    xs = x.cpu().numpy()
+    assert info["rel_residual"] < 1e-9
+    assert np.max(np.abs(xs[real] - 1.0)) < 1e-7
+    assert np.all(xs[~real] == 0.0)
