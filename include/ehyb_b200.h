@@ -157,6 +157,9 @@ typedef struct ehyb_dev_info {
   int32_t threads_per_cta;
   int32_t ctas;               /* grid size of one SpMV launch */
   int32_t sm_count;
+  int64_t pool_slices;        /* ER slices in the cross-CTA pool (0 = pool off) */
+  int32_t er_buf_slices;      /* own ER slices buffered in shared memory per CTA */
+  int32_t smem_bytes;         /* dynamic shared memory of a fused launch */
 } ehyb_dev_info;
 
 /* Upload an assembled matrix once (device = CUDA ordinal) and derive the
@@ -178,6 +181,7 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
 #define EHYB_TUNE_PREFETCH_ER 2
 #define EHYB_TUNE_THREADS 3
 #define EHYB_TUNE_TIMING 4
+#define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 4) */
 EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value);
 
 /* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].

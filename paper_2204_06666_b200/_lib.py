@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(PKG, "libehyb_b200.so")
 
 EINVAL, ENOMEM, ECUDA = 1, 2, 3
 MODE_STRICT, MODE_FMA = 0, 1
-TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING = 1, 2, 3, 4
+TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING, TUNE_ER_WARPS = 1, 2, 3, 4, 5
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -59,6 +59,7 @@ class DevInfo(C.Structure):
         ("device_bytes", C.c_int64), ("er_slices", C.c_int64), ("er_slots", C.c_int64),
         ("window_bytes", C.c_int64), ("window_in_smem", C.c_int32),
         ("threads_per_cta", C.c_int32), ("ctas", C.c_int32), ("sm_count", C.c_int32),
+        ("pool_slices", C.c_int64), ("er_buf_slices", C.c_int32), ("smem_bytes", C.c_int32),
     ]
 
 

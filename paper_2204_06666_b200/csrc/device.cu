@@ -101,7 +101,8 @@ struct ehyb_dev {
   void* yu = nullptr;
   // launch configuration
   int threads = 1024;
-  size_t smem = 0;
+  size_t smem = 0;      // dynamic smem of a fused launch (window + ER buffer)
+  size_t win_bytes = 0;  // window part
   bool window_in_smem = false, window_tma = false;
   int sm_count = 0;
   size_t bytes = 0;
@@ -114,6 +115,8 @@ struct ehyb_dev {
   unsigned int* chunk_flag = nullptr;
   unsigned int* pool_ctr = nullptr;
   unsigned int epoch = 0;
+  // own-ER shared-memory buffer
+  int er_buf_slices = 0, er_buf_offset = 0, er_warps = 4;
 
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
@@ -158,9 +161,15 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.chunk_flag = h->chunk_flag;
   P.chunk_pub = h->chunk_pub;
   P.epoch = h->epoch;
-  auto kern = P.window_in_smem ? spmv_fused_kernel<T, STRICT, C32, true>
+  P.er_buf_slices = h->er_buf_slices;
+  P.er_buf_offset = h->er_buf_offset;
+  P.er_warps = h->er_warps;
+  auto kern = (do_ell && h->window_in_smem) ? spmv_fused_kernel<T, STRICT, C32, true>
                               : spmv_fused_kernel<T, STRICT, C32, false>;
-  const size_t smem = P.window_in_smem ? h->smem : 0;
+  // dynamic smem: [window | own-ER buffer]; the buffer is only used when one
+  // launch runs both phases
+  const size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
+  if (!(do_ell && do_er)) P.er_buf_slices = 0;
   if (smem > 48 * 1024) {
     // opt in once per (kernel, device) to the largest window any handle needs
     static std::mutex mu;
@@ -288,9 +297,14 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   CUDA_TRY(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
   const size_t win = size_t(vec) * tb;
   const size_t win_al = (win + 127) / 128 * 128;
-  h->window_in_smem = win_al + 64 <= size_t(optin);
-  h->smem = h->window_in_smem ? win_al : 0;
+  constexpr size_t kStaticReserve = 2048;  // mbarrier, counters, done bitmaps
+  h->window_in_smem = win_al + kStaticReserve <= size_t(optin);
+  h->win_bytes = h->window_in_smem ? win_al : 0;
   h->window_tma = h->window_in_smem && (win % 16 == 0);  // TMA needs 16 B multiples
+  h->er_buf_offset = int(h->win_bytes);
+  h->er_buf_slices = int(std::min<size_t>(
+      kMaxErBuf, (size_t(optin) - h->win_bytes - kStaticReserve) / (32 * tb)));
+  h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
   const int64_t chunks = (vec + 31) / 32;
   h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(32, chunks * 32)));
   int per_sm = 0;
@@ -302,7 +316,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // its share of the mean per-CTA cost (ELL slots + er_cost * ER entries);
   // the rest joins a pool any CTA may claim once its own work is done
   const double pool_factor = env_double("EHYB_POOL_FACTOR", 0.95);
-  const double er_cost = env_double("EHYB_ER_COST", 3.0);
+  const double er_cost = env_double("EHYB_ER_COST", 5.0);
   std::vector<double> ell_cost(static_cast<size_t>(n_loc_parts)), er_total(static_cast<size_t>(n_loc_parts), 0.0);
   double total = 0.0;
   for (int64_t q = 0; q < n_loc_parts; ++q) {
@@ -348,6 +362,12 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     if (!any) break;
   }
   h->pool_hi = int64_t(order.size());
+  {
+    int64_t max_own = 0;
+    for (int64_t q = 0; q < n_loc_parts; ++q) max_own = std::max<int64_t>(max_own, int64_t(own[size_t(q)].size()));
+    h->er_buf_slices = int(std::min<int64_t>(h->er_buf_slices, max_own));
+    h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
+  }
   const int64_t n_sl = int64_t(order.size());
   std::vector<int64_t> epos(size_t(n_sl) + 1, 0);
   std::vector<int32_t> eswidth(size_t(n_sl), 0), erows(size_t(n_sl) * 32, -1),
@@ -474,6 +494,7 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
       if (value < 32 || value > 1024 || value % 32) return fail("threads must be a multiple of 32 in [32, 1024]");
       h->threads = int(value);
       return 0;
+    case EHYB_TUNE_ER_WARPS: h->er_warps = int(std::max<int64_t>(0, value)); return 0;
     case EHYB_TUNE_TIMING:
       h->timing = reinterpret_cast<unsigned long long*>(static_cast<uintptr_t>(value));
       return 0;
@@ -492,6 +513,9 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out) {
   out->threads_per_cta = h->threads;
   out->ctas = int32_t(h->local_rows / h->vec);
   out->sm_count = h->sm_count;
+  out->pool_slices = h->pool_hi - h->pool_lo;
+  out->er_buf_slices = h->er_buf_slices;
+  out->smem_bytes = int32_t(h->smem);
   return 0;
 }
 

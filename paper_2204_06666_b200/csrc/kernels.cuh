@@ -62,6 +62,10 @@ struct SpmvParams {
   unsigned int* chunk_flag;         // [n_chunks] epoch of the last published ELL chunk
   const uint32_t* __restrict__ chunk_pub;  // bitmap: chunk holds a pooled ER row
   unsigned int epoch;               // launch sequence number (>= 1)
+  // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
+  int32_t er_buf_slices;            // buffered own ER slices (<= kMaxErBuf)
+  int32_t er_buf_offset;            // byte offset of the buffer in dynamic smem
+  int32_t er_warps;                 // warps that start on ER before ELL
 };
 
 constexpr int32_t kPadFlag = 0x40000000;  // row had reference ER padding slots
@@ -140,33 +144,40 @@ __device__ __forceinline__ void prefetch_slice(const T* val, const uint16_t* col
 }
 
 // One 32-row SELL slice, one row per lane, slots pos + 32k. Full batches of
-// kUnroll slots issue all column and value loads before the first gather so
-// every lane keeps 2*kUnroll independent loads in flight; the tail batch is
-// predicated. The accumulation order is k ascending (reference order).
+// U slots issue all column and value loads before the first gather so every
+// lane keeps 2U independent loads in flight (U = 8 for fp64, 16 for fp32:
+// the same bytes in flight per lane); the tail batch is predicated. The
+// accumulation order is k ascending (reference order).
+template <typename T>
+struct EllUnroll {
+  static constexpr int value = sizeof(T) == 4 ? 16 : 8;
+};
+
 template <typename T, bool STRICT>
 __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
                                          const uint16_t* __restrict__ col, int64_t pos, int w,
                                          const T* win) {
+  constexpr int U = EllUnroll<T>::value;
   T acc = T(0);
   int k = 0;
-  for (; k + kUnroll <= w; k += kUnroll) {
-    uint32_t c[kUnroll];
-    T v[kUnroll];
+  for (; k + U <= w; k += U) {
+    uint32_t c[U];
+    T v[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
+    for (int u = 0; u < U; ++u) c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
-    T xv[kUnroll];
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
+    T xv[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) xv[u] = win[c[u]];
+    for (int u = 0; u < U; ++u) xv[u] = win[c[u]];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) acc = madd<STRICT>(acc, v[u], xv[u]);
+    for (int u = 0; u < U; ++u) acc = madd<STRICT>(acc, v[u], xv[u]);
   }
   if (k < w) {
-    uint32_t c[kUnroll];
-    T v[kUnroll];
+    uint32_t c[U];
+    T v[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       c[u] = 0;
       v[u] = T(0);
       if (k + u < w) {
@@ -175,7 +186,7 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
       }
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
+    for (int u = 0; u < U; ++u)
       if (k + u < w) acc = madd<STRICT>(acc, v[u], win[c[u]]);
   }
   return acc;
@@ -256,6 +267,7 @@ __device__ __forceinline__ int lds_volatile(const uint32_t* p, uint32_t bit) {
 }
 
 constexpr int kMaxChunks = EHYB_MAX_LOCAL_INDEX / 32;  // 32-row chunks per partition
+constexpr int kMaxErBuf = 2048;                        // buffered own ER slices per CTA
 
 // Fused EHYB SpMV, one CTA per partition.
 //   SMEM : the x window is staged in shared memory (else read from global)
@@ -270,7 +282,9 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   __shared__ uint64_t bar;
   __shared__ int next_chunk;
   __shared__ int next_er;
+  __shared__ int next_comb;
   __shared__ uint32_t chunk_done[kMaxChunks / 32];
+  __shared__ uint32_t er_done[kMaxErBuf / 32];
 
   const int part = blockIdx.x;
   const int64_t row0 = int64_t(part) * P.vec;
@@ -284,13 +298,15 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   const int64_t s1 = __ldg(P.er_part_ptr + part + 1);
 
   if (threadIdx.x == 0) {
-    next_chunk = nwarps;
-    next_er = nwarps;
+    next_chunk = 0;
+    next_er = 0;
+    next_comb = 0;
     if (P.timing) P.timing[4 * part] = globaltimer();
     if (part == 0 && P.pool_ctr) P.pool_ctr[(P.epoch + 1u) & 1u] = 0u;  // next launch's counter
   }
   for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
     chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
+  for (int i = threadIdx.x; i < kMaxErBuf / 32; i += blockDim.x) er_done[i] = 0u;
   if constexpr (SMEM) {
     if (P.window_tma) {
       if (threadIdx.x == 0) {
@@ -335,68 +351,107 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   const T* win = SMEM ? xs : xwin;
   if (P.timing && threadIdx.x == 0) P.timing[4 * part + 1] = globaltimer();
 
-  if (P.do_ell) {
-    int64_t chunk = wid;
-    while (chunk < n_chunks) {
-      if constexpr (C32) {
-        const int64_t s = (row0 >> 5) + chunk;
-        if (lane == 0 && P.pf_ell > 0 && chunk + P.pf_ell < n_chunks) {
-          const int64_t sp = s + P.pf_ell;
-          prefetch_slice(P.val_ell, P.col_ell, int64_t(__ldg(P.pos_ell + sp)),
-                         int64_t(__ldg(P.pos_ell + sp + 1)));
-        }
-        const int w = __ldg(P.width_ell + s);
-        const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + lane;
-        const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, pos, w, win);
-        P.y[row0 + chunk * 32 + lane] = acc;
-      } else {
-        const int64_t lr = chunk * 32 + lane;
-        if (lr < P.vec) {
-          const int64_t r = row0 + lr;
-          const int64_t C = P.warp;
-          const int64_t s = r / C;
-          const int w = __ldg(P.width_ell + s);
-          const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + (r - s * C);
-          P.y[r] = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
-        }
-      }
-      const int64_t gchunk = int64_t(part) * n_chunks + chunk;  // partition-major chunk id
-      const bool publish = P.chunk_pub && ((__ldg(P.chunk_pub + (gchunk >> 5)) >> (gchunk & 31)) & 1u);
-      if (publish) __threadfence();  // y of this chunk visible to other CTAs (pooled ER rows)
-      else __threadfence_block();
-      __syncwarp();
-      int nxt = 0;
-      if (lane == 0) {
-        if (publish) *reinterpret_cast<volatile unsigned int*>(P.chunk_flag + gchunk) = P.epoch;
-        atomicOr(&chunk_done[chunk >> 5], 1u << (chunk & 31));
-        nxt = atomicAdd(&next_chunk, 1);
-      }
-      chunk = __shfl_sync(0xffffffffu, nxt, 0);
+  // own ER slices [s0, s1): the first n_buf are computed into a shared-memory
+  // buffer at any time (ER-first warps overlap them with the ELL stream) and
+  // combined with y_ell at the end; the rest finish directly against y_ell
+  const int64_t n_own = s1 - s0;
+  const int64_t n_buf = (P.do_er && P.do_ell) ? (n_own < P.er_buf_slices ? n_own : P.er_buf_slices) : 0;
+  T* er_buf = reinterpret_cast<T*>(smem_raw + P.er_buf_offset);
+
+  auto claim = [&](int* ctr) -> int64_t {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  auto wait_chunk = [&](int64_t r) {
+    const int64_t ch = (r - row0) >> 5;
+    const uint32_t bit = 1u << (ch & 31);
+    while (!lds_volatile(&chunk_done[ch >> 5], bit)) {
     }
+    __threadfence_block();
+  };
+  auto run_chunk = [&](int64_t chunk) {
+    if constexpr (C32) {
+      const int64_t s = (row0 >> 5) + chunk;
+      if (lane == 0 && P.pf_ell > 0 && chunk + P.pf_ell < n_chunks) {
+        const int64_t sp = s + P.pf_ell;
+        prefetch_slice(P.val_ell, P.col_ell, int64_t(__ldg(P.pos_ell + sp)),
+                       int64_t(__ldg(P.pos_ell + sp + 1)));
+      }
+      const int w = __ldg(P.width_ell + s);
+      const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + lane;
+      const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, pos, w, win);
+      P.y[row0 + chunk * 32 + lane] = acc;
+    } else {
+      const int64_t lr = chunk * 32 + lane;
+      if (lr < P.vec) {
+        const int64_t r = row0 + lr;
+        const int64_t C = P.warp;
+        const int64_t s = r / C;
+        const int w = __ldg(P.width_ell + s);
+        const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + (r - s * C);
+        P.y[r] = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
+      }
+    }
+    const int64_t gchunk = int64_t(part) * n_chunks + chunk;  // partition-major chunk id
+    const bool publish = P.chunk_pub && ((__ldg(P.chunk_pub + (gchunk >> 5)) >> (gchunk & 31)) & 1u);
+    if (publish) __threadfence();  // y of this chunk visible to other CTAs (pooled ER rows)
+    else __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      if (publish) *reinterpret_cast<volatile unsigned int*>(P.chunk_flag + gchunk) = P.epoch;
+      atomicOr(&chunk_done[chunk >> 5], 1u << (chunk & 31));
+    }
+  };
+  auto run_own_er = [&](int64_t idx) {
+    int32_t rw;
+    const T acc = er_slice_acc<T, STRICT>(P, s0 + idx, s1, nwarps, lane, rw);
+    if (idx < n_buf) {
+      er_buf[idx * 32 + lane] = acc;
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) atomicOr(&er_done[idx >> 5], 1u << (idx & 31));
+    } else if (rw >= 0) {
+      const int64_t r = rw & kRowMask;
+      if (P.do_ell) wait_chunk(r);
+      P.y[r] = add_rn(__ldcg(P.y + r), acc);
+    }
+  };
+
+  int64_t pending = -1;
+  if (n_buf > 0 && wid < P.er_warps) {  // ER-first warps
+    for (;;) {
+      const int64_t idx = claim(&next_er);
+      if (idx >= n_buf) {
+        pending = idx;
+        break;
+      }
+      run_own_er(idx);
+    }
+  }
+  if (P.do_ell) {
+    int64_t chunk = claim(&next_chunk);
+    for (; chunk < n_chunks; chunk = claim(&next_chunk)) run_chunk(chunk);
     // first warp to find the ELL counter dry stamps the end of ELL issue
-    if (P.timing && lane == 0 && chunk == n_chunks + nwarps - 1)
-      P.timing[4 * part + 2] = globaltimer();
+    if (P.timing && lane == 0 && chunk == n_chunks) P.timing[4 * part + 2] = globaltimer();
   }
 
   if (P.do_er) {
-    // own ER rows: finish against this CTA's ELL chunks (shared-memory bits)
-    int64_t s = s0 + wid;
-    while (s < s1) {
-      int32_t rw;
-      T acc = er_slice_acc<T, STRICT>(P, s, s1, nwarps, lane, rw);
+    if (pending >= 0 && pending < n_own) run_own_er(pending);
+    for (int64_t idx = claim(&next_er); idx < n_own; idx = claim(&next_er)) run_own_er(idx);
+    // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
+    for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
+      while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
+      }
+      __threadfence_block();
+      const int32_t rw = __ldg(P.er_rows + (s0 + idx) * 32 + lane);
       if (rw >= 0) {
         const int64_t r = rw & kRowMask;
-        const int64_t ch = (r - row0) >> 5;
-        const uint32_t bit = 1u << (ch & 31);
-        while (!lds_volatile(&chunk_done[ch >> 5], bit)) {
-        }
-        __threadfence_block();
-        P.y[r] = add_rn(__ldcg(P.y + r), acc);
+        wait_chunk(r);
+        P.y[r] = add_rn(__ldcg(P.y + r), er_buf[idx * 32 + lane]);
       }
-      int nxt = 0;
-      if (lane == 0) nxt = atomicAdd(&next_er, 1);
-      s = s0 + __shfl_sync(0xffffffffu, nxt, 0);
     }
+    int64_t s;
     // shared pool: excess ER slices of heavy partitions, claimed by any CTA;
     // rows of other CTAs are finished once their ELL chunk is published
     if (P.pool_hi > P.pool_lo) {

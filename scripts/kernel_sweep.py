@@ -65,6 +65,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--pool", default="0,0.9,1.0,1.1")
     ap.add_argument("--er-cost", default="2.0")
+    ap.add_argument("--er-warps", default="0,4")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
     gold = bench.golden_y_digest(args.config)
@@ -85,17 +86,18 @@ def main():
         os.environ["EHYB_POOL_FACTOR"] = pool
         os.environ["EHYB_ER_COST"] = ercost
         handles[(pool, ercost)] = DeviceMatrix(e, 0)
+    ewl = [int(v) for v in args.er_warps.split(",")]
     for (pool, ercost), h in handles.items():
-        for pf, pfer in itertools.product([0] if args.quick else [0, 8], (0, 1)):
-            h.tune(prefetch_ell=pf, prefetch_er=pfer, threads=1024)
+        for pfer, ew in itertools.product((0, 1), ewl):
+            h.tune(prefetch_ell=0, prefetch_er=pfer, threads=1024, er_warps=ew)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
-            results.append(dict(pool=pool, er_cost=ercost, pf_ell=pf, pf_er=pfer,
+            results.append(dict(pool=pool, er_cost=ercost, pf_ell=0, pf_er=pfer, er_warps=ew,
                                 us=round(us, 2), gbs=round(bmin / us / 1e3, 1), bitwise=ok))
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
     dm = handles[(best["pool"], best["er_cost"])]
-    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024)
+    dm.tune(prefetch_ell=0, prefetch_er=best["pf_er"], threads=1024, er_warps=best["er_warps"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
     us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
     print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,

@@ -79,12 +79,26 @@ def test_corpus_bitwise():
         assert digest(y) == rec["y_reordered"], d["name"]
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg2", "cfg4"])
+_RGG_CACHE = {}
+
+
+def _config_matrix(name):
+    """cfg3f32 / cfg3f64 share one 5M-row matrix: generate it once."""
+    if name.startswith("cfg3f"):
+        if "m" not in _RGG_CACHE:
+            _RGG_CACHE["m"] = W.rgg3d(5_000_000)
+        n, r, c, v = _RGG_CACHE["m"]
+        return n, r, c, v, 4 if name == "cfg3f32" else 8
+    return W.build_config(name)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg2", "cfg4",
+                                  "cfg3f32", "cfg3f64"])
 def test_config_bitwise(name):
     rec = config_record(name)
     if rec is None:
         pytest.skip("golden record missing")
-    n, r, c, v, tau = W.build_config(name)
+    n, r, c, v, tau = _config_matrix(name)
     m, params, graph, parts, cls, plan, e = product_pipeline(n, r, c, v, tau, tuple(rec["profile"]))
     assert digest(e.val_ell) == rec["digests"]["val_ell"]
     x = W.deterministic_vector(n, 0)
