@@ -213,9 +213,18 @@ def config_block(args, m, e):
         "profile": "DeviceProfile(148, 32, 231424) (B200_PROFILE)",
         "n_parts": int(e.n_parts), "vec_cache_size": int(e.params.vec_cache_size),
         "nnz_ell": int(e.nnz_ell), "nnz_er": int(e.nnz_er),
-        "l2_policy": "inputs larger than L2 (matrix stream per step >> 126 MB L2)",
+        "l2_policy": ("inputs larger than L2 (matrix stream per step >= 2x the 126 MB L2)"
+                      if _min_bytes(e) >= 2 * 126e6 else
+                      "L2 flushed (512 MB write) before every timed step; L2-resident "
+                      "time reported separately"),
         "parallelism": f"one CTA per partition x{e.n_parts}",
     }
+
+
+def _min_bytes(e):
+    from paper_2204_06666_b200 import min_bytes
+
+    return min_bytes(e)
 
 
 def run_gpu(args):
@@ -226,7 +235,7 @@ def run_gpu(args):
     from golden_util import digest
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.dist:
         from paper_2204_06666_b200 import distributed as D
 
         return D.bench_main(args)
@@ -266,15 +275,41 @@ def run_gpu(args):
     stream.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # a step's matrix stream smaller than ~2x L2 would stay cache resident
+    # between back-to-back launches: flush L2 (write 512 MB) between steps and
+    # time each step on its own events
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_l2 = bmin < 2 * l2_bytes
+    t_resident = None
     with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            dm.spmv(xr, y, fma=args.fma, stream=stream)
-        ev1.record(stream)
-        ev1.synchronize()
+        if flush_l2:
+            scratch = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a, b in evs:
+                with torch.cuda.stream(stream):
+                    scratch.fill_(1)
+                a.record(stream)
+                dm.spmv(xr, y, fma=args.fma, stream=stream)
+                b.record(stream)
+            stream.synchronize()
+            t_step = sum(a.elapsed_time(b) for a, b in evs) / 1e3 / args.steps
+            ev0.record(stream)
+            for _ in range(args.steps):
+                dm.spmv(xr, y, fma=args.fma, stream=stream)
+            ev1.record(stream)
+            ev1.synchronize()
+            t_resident = ev0.elapsed_time(ev1) / 1e3 / args.steps
+            del scratch
+        else:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                dm.spmv(xr, y, fma=args.fma, stream=stream)
+            ev1.record(stream)
+            ev1.synchronize()
+            t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
         torch.cuda.synchronize()
-    t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
     value = flops / t_step / 1e9
     achieved = bmin / t_step / 1e9
     peak, peak_src = measured_peak()
@@ -361,6 +396,7 @@ def run_gpu(args):
         "parity": parity,
         "cusparse": cus,
         "kernel": {"avg_us": t_step * 1e6, "effective_gbs": achieved,
+                   "l2_resident_avg_us": None if t_resident is None else t_resident * 1e6,
                    "traffic_model_bytes": E.traffic_model(e), "device_info": info},
         "preprocessing": dict(prep_t, prep_to_spmv_ratio=(prep_t["partition_s"]
                                                           + prep_t["reorder_assemble_s"]) / t_step),
@@ -380,6 +416,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist", action="store_true",
+                    help="run the row-sharded (NCCL) path even on one GPU")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")

@@ -182,6 +182,7 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
 #define EHYB_TUNE_THREADS 3
 #define EHYB_TUNE_TIMING 4
 #define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 4) */
+#define EHYB_TUNE_CLAIM_AHEAD 6 /* bit0: ELL chunks, bit1: ER slices claimed one ahead */
 EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value);
 
 /* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(PKG, "libehyb_b200.so")
 EINVAL, ENOMEM, ECUDA = 1, 2, 3
 MODE_STRICT, MODE_FMA = 0, 1
 TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING, TUNE_ER_WARPS = 1, 2, 3, 4, 5
+TUNE_CLAIM_AHEAD = 6
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

@@ -111,17 +111,17 @@ struct ehyb_dev {
   unsigned long long* timing = nullptr;
   // ER pool (cross-CTA load balance)
   int64_t pool_lo = 0, pool_hi = 0;
-  uint32_t* chunk_pub = nullptr;
-  unsigned int* chunk_flag = nullptr;
+  unsigned int* part_flag = nullptr;
   unsigned int* pool_ctr = nullptr;
   unsigned int epoch = 0;
   // own-ER shared-memory buffer
   int er_buf_slices = 0, er_buf_offset = 0, er_warps = 4;
+  int ell_ahead = 0, er_ahead = 0;
 
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    chunk_pub, chunk_flag, pool_ctr};
+                    part_flag, pool_ctr};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -158,12 +158,13 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_lo = h->pool_lo;
   P.pool_hi = h->pool_hi;
   P.pool_ctr = h->pool_ctr;
-  P.chunk_flag = h->chunk_flag;
-  P.chunk_pub = h->chunk_pub;
+  P.part_flag = h->part_flag;
   P.epoch = h->epoch;
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
   P.er_warps = h->er_warps;
+  P.ell_ahead = h->ell_ahead;
+  P.er_ahead = h->er_ahead;
   auto kern = (do_ell && h->window_in_smem) ? spmv_fused_kernel<T, STRICT, C32, true>
                               : spmv_fused_kernel<T, STRICT, C32, false>;
   // dynamic smem: [window | own-ER buffer]; the buffer is only used when one
@@ -372,8 +373,6 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::vector<int64_t> epos(size_t(n_sl) + 1, 0);
   std::vector<int32_t> eswidth(size_t(n_sl), 0), erows(size_t(n_sl) * 32, -1),
       elwidth(size_t(n_sl) * 32, 0);
-  const int64_t n_chunk_total = n_loc_parts * chunks;
-  std::vector<uint32_t> pub(size_t((n_chunk_total + 31) / 32), 0u);
   for (int64_t sl = 0; sl < n_sl; ++sl) {
     const auto& ref = order[size_t(sl)];
     const auto& mem = members[size_t(ref.q)];
@@ -387,11 +386,6 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       erows[size_t(sl) * 32 + (i - ref.i0)] = row;
       elwidth[size_t(sl) * 32 + (i - ref.i0)] = w;
       eswidth[size_t(sl)] = std::max(eswidth[size_t(sl)], w);
-      if (sl >= h->pool_lo) {
-        const int64_t rq = lr / vec;
-        const int64_t gc = rq * chunks + ((lr - rq * vec) >> 5);
-        pub[size_t(gc >> 5)] |= 1u << (gc & 31);
-      }
     }
   }
   for (int64_t s = 0; s < n_sl; ++s) epos[size_t(s) + 1] = epos[size_t(s)] + 32 * int64_t(eswidth[size_t(s)]);
@@ -441,14 +435,13 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(upload(&h->inverse, inv.data(), inv.size() * 4, &h->bytes));
   }
 
-  // ---- ER pool state: claim counters and per-chunk publication epochs
+  // ---- ER pool state: claim counters and per-partition publication epochs
   if (h->pool_hi > h->pool_lo) {
-    CUDA_TRY(upload(&h->chunk_pub, pub.data(), pub.size() * 4, &h->bytes));
-    CUDA_TRY(cudaMalloc(&h->chunk_flag, size_t(n_chunk_total) * 4 + 16));
-    CUDA_TRY(cudaMemset(h->chunk_flag, 0, size_t(n_chunk_total) * 4 + 16));
+    CUDA_TRY(cudaMalloc(&h->part_flag, size_t(n_loc_parts) * 4 + 16));
+    CUDA_TRY(cudaMemset(h->part_flag, 0, size_t(n_loc_parts) * 4 + 16));
     CUDA_TRY(cudaMalloc(&h->pool_ctr, 16));
     CUDA_TRY(cudaMemset(h->pool_ctr, 0, 16));
-    h->bytes += size_t(n_chunk_total) * 4 + 32;
+    h->bytes += size_t(n_loc_parts) * 4 + 32;
   }
   *out = h.release();
   return 0;
@@ -495,6 +488,10 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
       h->threads = int(value);
       return 0;
     case EHYB_TUNE_ER_WARPS: h->er_warps = int(std::max<int64_t>(0, value)); return 0;
+    case EHYB_TUNE_CLAIM_AHEAD:
+      h->ell_ahead = int(value & 1);
+      h->er_ahead = int((value >> 1) & 1);
+      return 0;
     case EHYB_TUNE_TIMING:
       h->timing = reinterpret_cast<unsigned long long*>(static_cast<uintptr_t>(value));
       return 0;

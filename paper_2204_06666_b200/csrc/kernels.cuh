@@ -59,13 +59,14 @@ struct SpmvParams {
   // ER work pool shared by all CTAs (load balance across partitions)
   int64_t pool_lo, pool_hi;         // global slice range of the pool
   unsigned int* pool_ctr;           // [2] claim counters, alternating by epoch
-  unsigned int* chunk_flag;         // [n_chunks] epoch of the last published ELL chunk
-  const uint32_t* __restrict__ chunk_pub;  // bitmap: chunk holds a pooled ER row
+  unsigned int* part_flag;          // [n_parts] epoch whose ELL phase the partition published
   unsigned int epoch;               // launch sequence number (>= 1)
   // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
   int32_t er_buf_slices;            // buffered own ER slices (<= kMaxErBuf)
   int32_t er_buf_offset;            // byte offset of the buffer in dynamic smem
   int32_t er_warps;                 // warps that start on ER before ELL
+  int32_t ell_ahead;                // 1 = claim the next ELL chunk (and its metadata) one ahead
+  int32_t er_ahead;                 // 1 = same for ER slices
 };
 
 constexpr int32_t kPadFlag = 0x40000000;  // row had reference ER padding slots
@@ -124,6 +125,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
@@ -218,47 +228,51 @@ __device__ __forceinline__ T ell_row_generic(const T* __restrict__ val,
   return acc;
 }
 
-// One derived ER slice: lane row (-1 = empty lane) and its accumulated
-// products in k order, x read through the read-only path. `ahead` > 0 bulk-
-// prefetches the slice `ahead` positions later (same warp's likely next).
+// Derived ER slice metadata of one lane: target row (-1 = empty lane, with
+// kPadFlag), lane width, slice width and the lane's first slot.
+struct ErMeta {
+  int32_t rw;
+  int lw;
+  int sw;
+  int64_t pos;
+};
+
+template <typename T>
+__device__ __forceinline__ ErMeta er_slice_meta(const SpmvParams<T>& P, int64_t s, int lane) {
+  ErMeta m;
+  m.rw = __ldg(P.er_rows + s * 32 + lane);
+  m.lw = __ldg(P.er_lwidth + s * 32 + lane);
+  m.sw = __ldg(P.er_swidth + s);
+  m.pos = __ldg(P.er_pos + s) + lane;
+  return m;
+}
+
+// Products of one ER row in k order, x through the read-only path; the
+// reference's ER padding products 0*x[0] (engine.py:148-151) are inert for
+// finite x and NaN-propagating otherwise — reproduced with one product.
 template <typename T, bool STRICT>
-__device__ __forceinline__ T er_slice_acc(const SpmvParams<T>& P, int64_t s, int64_t s_end,
-                                          int ahead, int lane, int32_t& rw) {
-  rw = __ldg(P.er_rows + s * 32 + lane);
-  const int lw = __ldg(P.er_lwidth + s * 32 + lane);
-  const int sw = __ldg(P.er_swidth + s);
-  const int64_t pos = __ldg(P.er_pos + s) + lane;
-  if (lane == 0 && P.pf_er && ahead > 0 && s + ahead < s_end) {
-    const int64_t q = s + ahead;
-    const int64_t q0 = __ldg(P.er_pos + q), q1 = __ldg(P.er_pos + q + 1);
-    if (q1 > q0) {
-      bulk_prefetch_l2(P.er_val + q0, uint32_t((q1 - q0) * int64_t(sizeof(T))));
-      bulk_prefetch_l2(P.er_col + q0, uint32_t((q1 - q0) * 4));
-    }
-  }
+__device__ __forceinline__ T er_slice_compute(const SpmvParams<T>& P, const ErMeta& m) {
   T acc = T(0);
-  for (int k = 0; k < sw; k += kUnroll) {
+  for (int k = 0; k < m.sw; k += kUnroll) {
     T v[kUnroll];
     uint32_t c[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       c[u] = 0;
       v[u] = T(0);
-      if (k + u < lw) {
-        c[u] = __ldcs(P.er_col + pos + int64_t(k + u) * 32);
-        v[u] = __ldcs(P.er_val + pos + int64_t(k + u) * 32);
+      if (k + u < m.lw) {
+        c[u] = __ldcs(P.er_col + m.pos + int64_t(k + u) * 32);
+        v[u] = __ldcs(P.er_val + m.pos + int64_t(k + u) * 32);
       }
     }
     T xv[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) xv[u] = (k + u < lw) ? __ldg(P.x + c[u]) : T(0);
+    for (int u = 0; u < kUnroll; ++u) xv[u] = (k + u < m.lw) ? __ldg(P.x + c[u]) : T(0);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
-      if (k + u < lw) acc = madd<STRICT>(acc, v[u], xv[u]);
+      if (k + u < m.lw) acc = madd<STRICT>(acc, v[u], xv[u]);
   }
-  // reference ER padding products 0*x[0] (engine.py:148-151): inert for
-  // finite x, NaN-propagating otherwise — reproduced with one product
-  if (rw >= 0 && (rw & kPadFlag)) acc = add_rn(acc, mul_rn(T(0), __ldg(P.x)));
+  if (m.rw >= 0 && (m.rw & kPadFlag)) acc = add_rn(acc, mul_rn(T(0), __ldg(P.x)));
   return acc;
 }
 
@@ -283,6 +297,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   __shared__ int next_chunk;
   __shared__ int next_er;
   __shared__ int next_comb;
+  __shared__ int ell_finished;
   __shared__ uint32_t chunk_done[kMaxChunks / 32];
   __shared__ uint32_t er_done[kMaxErBuf / 32];
 
@@ -290,7 +305,6 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   const int64_t row0 = int64_t(part) * P.vec;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
   const int64_t n_chunks = (P.vec + 31) >> 5;
   T* xs = reinterpret_cast<T*>(smem_raw);
   const T* xwin = P.x + row0;
@@ -301,6 +315,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
     next_chunk = 0;
     next_er = 0;
     next_comb = 0;
+    ell_finished = 0;
     if (P.timing) P.timing[4 * part] = globaltimer();
     if (part == 0 && P.pool_ctr) P.pool_ctr[(P.epoch + 1u) & 1u] = 0u;  // next launch's counter
   }
@@ -370,49 +385,88 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
     }
     __threadfence_block();
   };
-  auto run_chunk = [&](int64_t chunk) {
-    if constexpr (C32) {
-      const int64_t s = (row0 >> 5) + chunk;
-      if (lane == 0 && P.pf_ell > 0 && chunk + P.pf_ell < n_chunks) {
-        const int64_t sp = s + P.pf_ell;
-        prefetch_slice(P.val_ell, P.col_ell, int64_t(__ldg(P.pos_ell + sp)),
-                       int64_t(__ldg(P.pos_ell + sp + 1)));
+  // per-chunk metadata, loaded one claim ahead so its latency overlaps the
+  // previous chunk's stream (narrow slices would otherwise pay two extra
+  // round trips per chunk)
+  struct EllMeta {
+    int w;
+    int64_t pos;
+  };
+  auto ell_meta = [&](int64_t chunk) -> EllMeta {
+    EllMeta m{0, 0};
+    if (chunk < n_chunks) {
+      if constexpr (C32) {
+        const int64_t s = (row0 >> 5) + chunk;
+        m.w = __ldg(P.width_ell + s);
+        m.pos = int64_t(__ldg(P.pos_ell + s));
+        if (lane == 0 && P.pf_ell > 0 && m.w > 0)  // precise L2 prefetch of the claimed chunk
+          prefetch_slice(P.val_ell, P.col_ell, m.pos, m.pos + 32 * int64_t(m.w));
       }
-      const int w = __ldg(P.width_ell + s);
-      const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + lane;
-      const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, pos, w, win);
+    }
+    return m;
+  };
+  // Chunk completion is published one chunk late: the CTA-scope fence that
+  // orders y[chunk] before its done bit runs after the warp has computed the
+  // NEXT chunk, when the earlier y store has long completed — a fence right
+  // after the store would stall the warp for a full store round trip.
+  int64_t unpublished = -1;
+  auto publish = [&]() {
+    if (unpublished < 0) return;
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      atomicOr(&chunk_done[unpublished >> 5], 1u << (unpublished & 31));
+      // the warp publishing the partition's last chunk publishes the whole
+      // ELL phase to other CTAs (pooled ER rows): one gpu-scope fence per
+      // CTA instead of one per chunk
+      if (P.part_flag && atomicAdd(&ell_finished, 1) == int(n_chunks) - 1) {
+        __threadfence();
+        st_release_gpu(P.part_flag + part, P.epoch);
+      }
+    }
+    unpublished = -1;
+  };
+  auto run_chunk = [&](int64_t chunk, const EllMeta& m) {
+    if constexpr (C32) {
+      const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, m.pos + lane, m.w, win);
+      publish();
       P.y[row0 + chunk * 32 + lane] = acc;
     } else {
       const int64_t lr = chunk * 32 + lane;
+      T acc = T(0);
       if (lr < P.vec) {
         const int64_t r = row0 + lr;
         const int64_t C = P.warp;
         const int64_t s = r / C;
         const int w = __ldg(P.width_ell + s);
         const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + (r - s * C);
-        P.y[r] = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
+        acc = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
+      }
+      publish();
+      if (lr < P.vec) P.y[row0 + lr] = acc;
+    }
+    unpublished = chunk;
+  };
+  auto er_meta = [&](int64_t s, int64_t s_end) -> ErMeta {
+    ErMeta m{-1, 0, 0, 0};
+    if (s < s_end) {
+      m = er_slice_meta(P, s, lane);
+      if (lane == 0 && P.pf_er && m.sw > 0) {  // precise L2 prefetch of the claimed slice
+        bulk_prefetch_l2(P.er_val + m.pos - lane, uint32_t(32 * int64_t(m.sw) * int64_t(sizeof(T))));
+        bulk_prefetch_l2(P.er_col + m.pos - lane, uint32_t(32 * int64_t(m.sw) * 4));
       }
     }
-    const int64_t gchunk = int64_t(part) * n_chunks + chunk;  // partition-major chunk id
-    const bool publish = P.chunk_pub && ((__ldg(P.chunk_pub + (gchunk >> 5)) >> (gchunk & 31)) & 1u);
-    if (publish) __threadfence();  // y of this chunk visible to other CTAs (pooled ER rows)
-    else __threadfence_block();
-    __syncwarp();
-    if (lane == 0) {
-      if (publish) *reinterpret_cast<volatile unsigned int*>(P.chunk_flag + gchunk) = P.epoch;
-      atomicOr(&chunk_done[chunk >> 5], 1u << (chunk & 31));
-    }
+    return m;
   };
-  auto run_own_er = [&](int64_t idx) {
-    int32_t rw;
-    const T acc = er_slice_acc<T, STRICT>(P, s0 + idx, s1, nwarps, lane, rw);
+  auto finish_own_er = [&](int64_t idx, const ErMeta& m) {
+    const T acc = er_slice_compute<T, STRICT>(P, m);
     if (idx < n_buf) {
       er_buf[idx * 32 + lane] = acc;
       __threadfence_block();
       __syncwarp();
       if (lane == 0) atomicOr(&er_done[idx >> 5], 1u << (idx & 31));
-    } else if (rw >= 0) {
-      const int64_t r = rw & kRowMask;
+    } else if (m.rw >= 0) {
+      const int64_t r = m.rw & kRowMask;
       if (P.do_ell) wait_chunk(r);
       P.y[r] = add_rn(__ldcg(P.y + r), acc);
     }
@@ -426,19 +480,44 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
         pending = idx;
         break;
       }
-      run_own_er(idx);
+      finish_own_er(idx, er_meta(s0 + idx, s1));
     }
   }
   if (P.do_ell) {
     int64_t chunk = claim(&next_chunk);
-    for (; chunk < n_chunks; chunk = claim(&next_chunk)) run_chunk(chunk);
-    // first warp to find the ELL counter dry stamps the end of ELL issue
+    if (P.ell_ahead) {
+      EllMeta m = ell_meta(chunk);
+      while (chunk < n_chunks) {
+        const int64_t nxt = claim(&next_chunk);
+        const EllMeta mn = ell_meta(nxt);
+        run_chunk(chunk, m);
+        chunk = nxt;
+        m = mn;
+      }
+    } else {
+      for (; chunk < n_chunks; chunk = claim(&next_chunk)) run_chunk(chunk, ell_meta(chunk));
+    }
+    publish();  // this warp's last chunk
+    // the warp whose claim first ran past the end stamps the end of ELL issue
     if (P.timing && lane == 0 && chunk == n_chunks) P.timing[4 * part + 2] = globaltimer();
   }
 
   if (P.do_er) {
-    if (pending >= 0 && pending < n_own) run_own_er(pending);
-    for (int64_t idx = claim(&next_er); idx < n_own; idx = claim(&next_er)) run_own_er(idx);
+    if (pending >= 0 && pending < n_own) finish_own_er(pending, er_meta(s0 + pending, s1));
+    if (P.er_ahead) {
+      int64_t idx = claim(&next_er);
+      ErMeta m = er_meta(s0 + idx, s1);
+      while (idx < n_own) {
+        const int64_t nxt = claim(&next_er);
+        const ErMeta mn = er_meta(s0 + nxt, s1);
+        finish_own_er(idx, m);
+        idx = nxt;
+        m = mn;
+      }
+    } else {
+      for (int64_t idx = claim(&next_er); idx < n_own; idx = claim(&next_er))
+        finish_own_er(idx, er_meta(s0 + idx, s1));
+    }
     // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
     for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
       while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
@@ -451,30 +530,31 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
         P.y[r] = add_rn(__ldcg(P.y + r), er_buf[idx * 32 + lane]);
       }
     }
-    int64_t s;
     // shared pool: excess ER slices of heavy partitions, claimed by any CTA;
     // rows of other CTAs are finished once their ELL chunk is published
     if (P.pool_hi > P.pool_lo) {
       unsigned int* ctr = P.pool_ctr + (P.epoch & 1u);
-      int64_t idx = 0;
-      if (lane == 0) idx = atomicAdd(ctr, 1u);
-      s = P.pool_lo + __shfl_sync(0xffffffffu, idx, 0);
+      auto pclaim = [&]() -> int64_t {
+        unsigned int v = 0;
+        if (lane == 0) v = atomicAdd(ctr, 1u);
+        return P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
+      };
+      int64_t s = pclaim();
+      ErMeta m = er_meta(s, P.pool_hi);
       while (s < P.pool_hi) {
-        int32_t rw;
-        T acc = er_slice_acc<T, STRICT>(P, s, P.pool_hi, 0, lane, rw);
-        if (rw >= 0) {
-          const int64_t r = rw & kRowMask;
-          if (P.do_ell) {
-            const int64_t rp = r / P.vec;
-            const volatile unsigned int* f =
-                P.chunk_flag + rp * ((P.vec + 31) >> 5) + ((r - rp * P.vec) >> 5);
-            while (*f != P.epoch) __nanosleep(64);
-            __threadfence();
+        const int64_t nxt = pclaim();
+        const ErMeta mn = er_meta(nxt, P.pool_hi);
+        const T acc = er_slice_compute<T, STRICT>(P, m);
+        if (m.rw >= 0) {
+          const int64_t r = m.rw & kRowMask;
+          if (P.do_ell) {  // the owning CTA's ELL phase must be published
+            const uint32_t rp = uint32_t(r) / uint32_t(P.vec);
+            while (ld_acquire_gpu(P.part_flag + rp) != P.epoch) __nanosleep(64);
           }
           P.y[r] = add_rn(__ldcg(P.y + r), acc);
         }
-        if (lane == 0) idx = atomicAdd(ctr, 1u);
-        s = P.pool_lo + __shfl_sync(0xffffffffu, idx, 0);
+        s = nxt;
+        m = mn;
       }
     }
   }

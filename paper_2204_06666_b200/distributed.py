@@ -311,8 +311,11 @@ def bench_main(args):
     from .format import b200_profile, build_ehyb
     from .matrix_io import CooMatrix, read_ehyb_container, write_ehyb_container
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"),
+                 ("WORLD_SIZE", "1")):
+        os.environ.setdefault(k, v)  # allow a single-process run without torchrun
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))

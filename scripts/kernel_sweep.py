@@ -66,6 +66,8 @@ def main():
     ap.add_argument("--pool", default="0,0.9,1.0,1.1")
     ap.add_argument("--er-cost", default="2.0")
     ap.add_argument("--er-warps", default="0,4")
+    ap.add_argument("--ahead", default="0,3")
+    ap.add_argument("--pf-ell", default="0,1")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
     gold = bench.golden_y_digest(args.config)
@@ -87,17 +89,21 @@ def main():
         os.environ["EHYB_ER_COST"] = ercost
         handles[(pool, ercost)] = DeviceMatrix(e, 0)
     ewl = [int(v) for v in args.er_warps.split(",")]
+    ahl = [int(v) for v in args.ahead.split(",")]
+    pfl = [int(v) for v in args.pf_ell.split(",")]
     for (pool, ercost), h in handles.items():
-        for pfer, ew in itertools.product((0, 1), ewl):
-            h.tune(prefetch_ell=0, prefetch_er=pfer, threads=1024, er_warps=ew)
+        for pfer, ew, ah, pfe in itertools.product((0, 1), ewl, ahl, pfl):
+            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
-            results.append(dict(pool=pool, er_cost=ercost, pf_ell=0, pf_er=pfer, er_warps=ew,
-                                us=round(us, 2), gbs=round(bmin / us / 1e3, 1), bitwise=ok))
+            results.append(dict(pool=pool, er_cost=ercost, pf_ell=pfe, pf_er=pfer, er_warps=ew,
+                                ahead=ah, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
+                                bitwise=ok))
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
     dm = handles[(best["pool"], best["er_cost"])]
-    dm.tune(prefetch_ell=0, prefetch_er=best["pf_er"], threads=1024, er_warps=best["er_warps"])
+    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024,
+            er_warps=best["er_warps"], claim_ahead=best["ahead"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
     us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
     print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,
