@@ -183,6 +183,7 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
 #define EHYB_TUNE_TIMING 4
 #define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 4) */
 #define EHYB_TUNE_CLAIM_AHEAD 6 /* bit0: ELL chunks, bit1: ER slices claimed one ahead */
+#define EHYB_TUNE_ER_MIX 7 /* 1 = buffered own ER slices interleaved with ELL chunks */
 EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value);
 
 /* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].
@@ -207,6 +208,17 @@ EHYB_API int ehyb_dev_spmv_user(ehyb_dev* h, const void* x_user, void* y_user, i
  * Host buffers may be pageable or pinned (pinned is faster). */
 EHYB_API int ehyb_dev_spmv_host(ehyb_dev* h, const void* x_host, void* y_host, int user_order,
                                 int mode, void* stream);
+
+/* A sequence of independent products from HOST memory (the same call as
+ * ehyb_dev_spmv_host repeated `count` times: vector i is x_hosts[i] ->
+ * y_hosts[i], user_order as above), pipelined on two device buffer pairs:
+ * the copy-in of vector i+1 and the copy-out of vector i-1 overlap the
+ * product of vector i (copy-in / copy-out on handle-owned streams, compute on
+ * `stream`). Returns after the last copy-out; host buffers should be pinned.
+ * Results are bitwise those of count single calls. */
+EHYB_API int ehyb_dev_spmv_host_many(ehyb_dev* h, const void* const* x_hosts,
+                                     void* const* y_hosts, int64_t count, int user_order,
+                                     int mode, void* stream);
 
 /* ------------------------------------------- cuSPARSE CSR comparator */
 typedef struct ehyb_csr ehyb_csr;

@@ -21,6 +21,7 @@ EINVAL, ENOMEM, ECUDA = 1, 2, 3
 MODE_STRICT, MODE_FMA = 0, 1
 TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING, TUNE_ER_WARPS = 1, 2, 3, 4, 5
 TUNE_CLAIM_AHEAD = 6
+TUNE_ER_MIX = 7
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -106,6 +107,8 @@ _PROTOS = {
     "ehyb_dev_unpermute": (C.c_int, [vp, vp, vp, vp]),
     "ehyb_dev_spmv_user": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     "ehyb_dev_spmv_host": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
+    "ehyb_dev_spmv_host_many": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                          C.c_int64, C.c_int, C.c_int, vp]),
     "ehyb_dev_gather": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int32, vp]),
     "ehyb_dev_dot": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp, vp]),
     "ehyb_dev_cg_xr": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp]),

@@ -116,14 +116,28 @@ struct ehyb_dev {
   unsigned int epoch = 0;
   // own-ER shared-memory buffer
   int er_buf_slices = 0, er_buf_offset = 0, er_warps = 4;
-  int ell_ahead = 0, er_ahead = 0;
+  int ell_ahead = 0, er_ahead = 0, er_mix = 0;
+  // host-batch pipeline (ehyb_dev_spmv_host_many): copy-in / copy-out streams,
+  // two device buffer pairs, per-buffer events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
+              ev_out[2] = {nullptr, nullptr};
+  void* bx[2] = {nullptr, nullptr};
+  void* by[2] = {nullptr, nullptr};
 
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    part_flag, pool_ctr};
+                    part_flag, pool_ctr, bx[0], bx[1], by[0], by[1]};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    for (int b = 0; b < 2; ++b) {
+      if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+      if (ev_comp[b]) cudaEventDestroy(ev_comp[b]);
+      if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+    }
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
   }
 };
 
@@ -165,12 +179,16 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.er_warps = h->er_warps;
   P.ell_ahead = h->ell_ahead;
   P.er_ahead = h->er_ahead;
+  P.er_mix = h->er_mix;
   auto kern = (do_ell && h->window_in_smem) ? spmv_fused_kernel<T, STRICT, C32, true>
                               : spmv_fused_kernel<T, STRICT, C32, false>;
   // dynamic smem: [window | own-ER buffer]; the buffer is only used when one
   // launch runs both phases
   const size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
-  if (!(do_ell && do_er)) P.er_buf_slices = 0;
+  if (!(do_ell && do_er)) {
+    P.er_buf_slices = 0;
+    P.er_mix = 0;
+  }
   if (smem > 48 * 1024) {
     // opt in once per (kernel, device) to the largest window any handle needs
     static std::mutex mu;
@@ -492,6 +510,7 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
       h->ell_ahead = int(value & 1);
       h->er_ahead = int((value >> 1) & 1);
       return 0;
+    case EHYB_TUNE_ER_MIX: h->er_mix = value ? 1 : 0; return 0;
     case EHYB_TUNE_TIMING:
       h->timing = reinterpret_cast<unsigned long long*>(static_cast<uintptr_t>(value));
       return 0;
@@ -633,6 +652,69 @@ EHYB_API int ehyb_dev_spmv_host(ehyb_dev* h, const void* x_host, void* y_host, i
       CUDA_TRY(launch_spmv(h, h->xr, h->yr, mode, true, true, st));
       CUDA_TRY(cudaMemcpyAsync(y_host, h->yr, pb, cudaMemcpyDeviceToHost, st));
     }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+static int ensure_pipeline(ehyb_dev* h) {
+  if (h->s_in) return 0;
+  const size_t pb = size_t(h->padded) * size_t(h->tau);
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(cudaMalloc(&h->bx[b], pb));
+    CUDA_TRY(cudaMalloc(&h->by[b], pb));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_comp[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming));
+  }
+  h->bytes += 4 * pb;
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+  return 0;
+}
+
+EHYB_API int ehyb_dev_spmv_host_many(ehyb_dev* h, const void* const* x_hosts,
+                                     void* const* y_hosts, int64_t count, int user_order,
+                                     int mode, void* stream) {
+  EHYB_TRY {
+    if (!h || h->shard) return fail("spmv_host_many needs a full-matrix handle");
+    if (count < 0 || (count > 0 && (!x_hosts || !y_hosts))) return fail("null argument");
+    if (count == 0) return 0;
+    DeviceGuard guard(h->device);
+    int rc = ensure_scratch(h);
+    if (rc) return rc;
+    rc = ensure_pipeline(h);
+    if (rc) return rc;
+    auto st = static_cast<cudaStream_t>(stream);
+    const size_t tb = size_t(h->tau);
+    const size_t nb = size_t(user_order ? h->dimension : h->padded) * tb;
+    // the copy-in stream starts after whatever the caller queued on `st`
+    cudaEvent_t ev_start = h->ev_out[0];
+    CUDA_TRY(cudaEventRecord(ev_start, st));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
+    for (int64_t i = 0; i < count; ++i) {
+      const int b = int(i & 1);
+      // copy-in: buffer b is free once the compute of vector i-2 has read it
+      if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_comp[b], 0));
+      CUDA_TRY(cudaMemcpyAsync(h->bx[b], x_hosts[i], nb, cudaMemcpyHostToDevice, h->s_in));
+      CUDA_TRY(cudaEventRecord(h->ev_in[b], h->s_in));
+      // compute on the caller's stream; by[b] is free once the copy-out of i-2 ended
+      CUDA_TRY(cudaStreamWaitEvent(st, h->ev_in[b], 0));
+      if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_out[b], 0));
+      if (user_order) {
+        rc = ehyb_dev_spmv_user(h, h->bx[b], h->by[b], mode, stream);
+        if (rc) return rc;
+      } else {
+        CUDA_TRY(launch_spmv(h, h->bx[b], h->by[b], mode, true, true, st));
+      }
+      CUDA_TRY(cudaEventRecord(h->ev_comp[b], st));
+      // copy-out overlaps the next vector's copy-in (PCIe is full duplex)
+      CUDA_TRY(cudaStreamWaitEvent(h->s_out, h->ev_comp[b], 0));
+      CUDA_TRY(cudaMemcpyAsync(y_hosts[i], h->by[b], nb, cudaMemcpyDeviceToHost, h->s_out));
+      CUDA_TRY(cudaEventRecord(h->ev_out[b], h->s_out));
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->s_out));
     CUDA_TRY(cudaStreamSynchronize(st));
     return 0;
   }

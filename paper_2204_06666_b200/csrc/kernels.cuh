@@ -67,6 +67,7 @@ struct SpmvParams {
   int32_t er_warps;                 // warps that start on ER before ELL
   int32_t ell_ahead;                // 1 = claim the next ELL chunk (and its metadata) one ahead
   int32_t er_ahead;                 // 1 = same for ER slices
+  int32_t er_mix;                   // 1 = own buffered ER slices interleaved with ELL chunks
 };
 
 constexpr int32_t kPadFlag = 0x40000000;  // row had reference ER padding slots
@@ -166,7 +167,7 @@ struct EllUnroll {
 template <typename T, bool STRICT>
 __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
                                          const uint16_t* __restrict__ col, int64_t pos, int w,
-                                         const T* win) {
+                                         const T* win, uint64_t* win_bar) {
   constexpr int U = EllUnroll<T>::value;
   T acc = T(0);
   int k = 0;
@@ -177,6 +178,12 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
     for (int u = 0; u < U; ++u) c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
+    // a warp's first chunk issues its stream loads before the window has
+    // landed: the TMA copy and the first HBM round trip overlap
+    if (win_bar) {
+      mbar_wait(win_bar, 0);
+      win_bar = nullptr;
+    }
     T xv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) xv[u] = win[c[u]];
@@ -195,6 +202,7 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
         v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
       }
     }
+    if (win_bar) mbar_wait(win_bar, 0);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + u < w) acc = madd<STRICT>(acc, v[u], win[c[u]]);
@@ -313,7 +321,10 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
 
   if (threadIdx.x == 0) {
     next_chunk = 0;
-    next_er = 0;
+    next_er = (P.er_mix && P.do_er && P.do_ell)
+                  ? int(min(int64_t(P.er_buf_slices),
+                            int64_t(__ldg(P.er_part_ptr + part + 1) - __ldg(P.er_part_ptr + part))))
+                  : 0;
     next_comb = 0;
     ell_finished = 0;
     if (P.timing) P.timing[4 * part] = globaltimer();
@@ -355,16 +366,20 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
       }
     }
   }
+  // C32: each warp waits for the window inside its first ELL chunk, after
+  // that chunk's loads are in flight (ell_slice32)
+  bool win_pending = false;
   if constexpr (SMEM) {
     if (P.window_tma) {
-      mbar_wait(&bar, 0);
+      if constexpr (C32) win_pending = true;
+      else mbar_wait(&bar, 0);
     } else {
       for (int64_t i = threadIdx.x; i < P.vec; i += blockDim.x) xs[i] = xwin[i];
       __syncthreads();
     }
   }
   const T* win = SMEM ? xs : xwin;
-  if (P.timing && threadIdx.x == 0) P.timing[4 * part + 1] = globaltimer();
+  if (P.timing && threadIdx.x == 0 && !win_pending) P.timing[4 * part + 1] = globaltimer();
 
   // own ER slices [s0, s1): the first n_buf are computed into a shared-memory
   // buffer at any time (ER-first warps overlap them with the ELL stream) and
@@ -428,7 +443,12 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   };
   auto run_chunk = [&](int64_t chunk, const EllMeta& m) {
     if constexpr (C32) {
-      const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, m.pos + lane, m.w, win);
+      const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, m.pos + lane, m.w, win,
+                                           (SMEM && win_pending) ? &bar : nullptr);
+      if (SMEM && win_pending) {
+        win_pending = false;
+        if (P.timing && threadIdx.x == 0) P.timing[4 * part + 1] = globaltimer();
+      }
       publish();
       P.y[row0 + chunk * 32 + lane] = acc;
     } else {
@@ -473,7 +493,25 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   };
 
   int64_t pending = -1;
-  if (n_buf > 0 && wid < P.er_warps) {  // ER-first warps
+  const bool mix = P.er_mix && n_buf > 0;
+  if (mix) {
+    // one shared item sequence: the n_buf buffered own ER slices spread evenly
+    // among the n_chunks ELL chunks, so their gather latency hides behind the
+    // ELL stream of the other warps; item t is ER slice floor(t*n_buf/total)
+    // when that floor steps at t, else ELL chunk t - floor(t*n_buf/total)
+    const int64_t total = n_chunks + n_buf;
+    for (int64_t t = claim(&next_chunk); t < total; t = claim(&next_chunk)) {
+      const int64_t e0 = (t * n_buf) / total;
+      if (((t + 1) * n_buf) / total > e0) {
+        finish_own_er(e0, er_meta(s0 + e0, s1));
+        publish();
+      } else {
+        run_chunk(t - e0, ell_meta(t - e0));
+      }
+      if (P.timing && lane == 0 && t + 1 == total) P.timing[4 * part + 2] = globaltimer();
+    }
+    publish();
+  } else if (n_buf > 0 && wid < P.er_warps) {  // ER-first warps
     for (;;) {
       const int64_t idx = claim(&next_er);
       if (idx >= n_buf) {
@@ -483,7 +521,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
       finish_own_er(idx, er_meta(s0 + idx, s1));
     }
   }
-  if (P.do_ell) {
+  if (P.do_ell && !mix) {
     int64_t chunk = claim(&next_chunk);
     if (P.ell_ahead) {
       EllMeta m = ell_meta(chunk);

@@ -69,7 +69,7 @@ class DeviceMatrix:
 
     def tune(self, *, prefetch_ell: int | None = None, prefetch_er: bool | None = None,
              threads: int | None = None, timing=False, er_warps: int | None = None,
-             claim_ahead: int | None = None) -> None:
+             claim_ahead: int | None = None, er_mix: bool | None = None) -> None:
         """Launch knobs (include/ehyb_b200.h ehyb_dev_tune). `timing`: a CUDA
         int64 tensor of n_ctas*4 entries to record per-CTA stamps, None to
         stop recording, False (default) to leave it unchanged."""
@@ -83,6 +83,8 @@ class DeviceMatrix:
             L.call("ehyb_dev_tune", self._h, L.TUNE_ER_WARPS, int(er_warps))
         if claim_ahead is not None:
             L.call("ehyb_dev_tune", self._h, L.TUNE_CLAIM_AHEAD, int(claim_ahead))
+        if er_mix is not None:
+            L.call("ehyb_dev_tune", self._h, L.TUNE_ER_MIX, int(bool(er_mix)))
         if timing is not False:
             ptr = 0 if timing is None else int(timing.data_ptr())
             L.call("ehyb_dev_tune", self._h, L.TUNE_TIMING, ptr)
@@ -166,6 +168,41 @@ class DeviceMatrix:
                1 if user_order else 0, L.MODE_FMA if fma else L.MODE_STRICT,
                _stream_ptr(None, self.device))
         return y
+
+    def spmv_host_many(self, xs, *, user_order: bool, fma: bool = False, out=None):
+        """Independent products of several host vectors (ehyb_dev_spmv_host_many):
+        each is copied in, multiplied and copied out like `spmv_host`, but the
+        copy-in of the next vector and the copy-out of the previous one overlap
+        the current product. `xs`: a sequence of 1-D arrays or a 2-D array (one
+        vector per row); `out`: matching output arrays (allocated if None).
+        Pinned (page-locked) host arrays give the full PCIe rate."""
+        length = self.dimension if user_order else self.padded
+        xs = [xs[i] for i in range(len(xs))]
+        for i, x in enumerate(xs):
+            if not (isinstance(x, np.ndarray) and x.dtype == self.dtype and x.ndim == 1
+                    and x.flags.c_contiguous):
+                x = np.ascontiguousarray(x, dtype=self.dtype)
+                xs[i] = x
+            if x.ndim != 1 or x.size != length:
+                raise ValueError("length mismatch: x must have "
+                                 + ("the matrix dimension" if user_order
+                                    else "padded_dimension entries"))
+        if out is None:
+            out = [np.empty(length, dtype=self.dtype) for _ in xs]
+        ys = [out[i] for i in range(len(out))]
+        if len(ys) != len(xs):
+            raise ValueError("length mismatch: one output per input vector")
+        for y in ys:
+            if not (isinstance(y, np.ndarray) and y.dtype == self.dtype and y.ndim == 1
+                    and y.size == length and y.flags.c_contiguous and y.flags.writeable):
+                raise ValueError(f"length mismatch: outputs must be writable contiguous "
+                                 f"{np.dtype(self.dtype).name} arrays of {length} entries")
+        k = len(xs)
+        xp = (C.c_void_p * max(k, 1))(*[x.ctypes.data for x in xs])
+        yp = (C.c_void_p * max(k, 1))(*[y.ctypes.data for y in ys])
+        L.call("ehyb_dev_spmv_host_many", self._h, xp, yp, k, 1 if user_order else 0,
+               L.MODE_FMA if fma else L.MODE_STRICT, _stream_ptr(None, self.device))
+        return out
 
 
 def device_matrix(e: EhybMatrix, device: int | None = None) -> DeviceMatrix:

@@ -68,6 +68,8 @@ def main():
     ap.add_argument("--er-warps", default="0,4")
     ap.add_argument("--ahead", default="0,3")
     ap.add_argument("--pf-ell", default="0,1")
+    ap.add_argument("--mix", default="0,1")
+    ap.add_argument("--pf-er", default="0,1")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
     gold = bench.golden_y_digest(args.config)
@@ -91,19 +93,24 @@ def main():
     ewl = [int(v) for v in args.er_warps.split(",")]
     ahl = [int(v) for v in args.ahead.split(",")]
     pfl = [int(v) for v in args.pf_ell.split(",")]
+    mxl = [int(v) for v in args.mix.split(",")]
+    pfrl = [int(v) for v in args.pf_er.split(",")]
     for (pool, ercost), h in handles.items():
-        for pfer, ew, ah, pfe in itertools.product((0, 1), ewl, ahl, pfl):
-            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah)
+        for pfer, ew, ah, pfe, mx in itertools.product(pfrl, ewl, ahl, pfl, mxl):
+            if mx and ew != ewl[0]:
+                continue  # er_warps is unused in mix mode
+            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah,
+                   er_mix=mx)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
             results.append(dict(pool=pool, er_cost=ercost, pf_ell=pfe, pf_er=pfer, er_warps=ew,
-                                ahead=ah, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
+                                ahead=ah, mix=mx, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
                                 bitwise=ok))
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
     dm = handles[(best["pool"], best["er_cost"])]
     dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024,
-            er_warps=best["er_warps"], claim_ahead=best["ahead"])
+            er_warps=best["er_warps"], claim_ahead=best["ahead"], er_mix=best["mix"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
     us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
     print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,

@@ -180,3 +180,30 @@ def test_edge_cases():
         E.spmv_ehyb(e, np.zeros(3))
     with pytest.raises(ValueError, match="length mismatch"):
         E.spmv_ehyb_user(e, np.zeros(n + 1))
+
+
+@pytest.mark.parametrize("user_order", [True, False])
+def test_host_many_pipeline_matches_single_calls(user_order):
+    # the pipelined host path (copy-in / product / copy-out of neighbouring
+    # vectors overlapped) gives each vector exactly the single-call result
+    n, r, c, v = W.permute_symmetric(*W.stencil27(24, 24, 24), seed=5)
+    m = E.CooMatrix(n, n, r, c, v)
+    e = E.build_ehyb(m, tau=8, profile=E.DeviceProfile(12, 32, 16384))
+    dm = E.device_matrix(e, 0)
+    length = n if user_order else e.padded_dimension
+    xs = [torch.from_numpy(W.deterministic_vector(length, s)).pin_memory().numpy()
+          for s in range(7)]
+    ys = [torch.empty(length, dtype=torch.float64).pin_memory().numpy() for _ in xs]
+    out = dm.spmv_host_many(xs, user_order=user_order, out=ys)
+    assert out is ys
+    for x, y in zip(xs, ys):
+        want = dm.spmv_host(x, user_order=user_order)
+        assert y.tobytes() == want.tobytes()
+    # pageable inputs, a 2-D batch, and the empty batch
+    X = np.stack([W.deterministic_vector(length, 9 + s) for s in range(3)])
+    Y = dm.spmv_host_many(X, user_order=user_order)
+    for x, y in zip(X, Y):
+        assert y.tobytes() == dm.spmv_host(x, user_order=user_order).tobytes()
+    assert dm.spmv_host_many([], user_order=user_order) == []
+    with pytest.raises(ValueError, match="length mismatch"):
+        dm.spmv_host_many([np.zeros(3)], user_order=user_order)
