@@ -238,7 +238,7 @@ def run_gpu(args):
     if world > 1 or args.gpus > 1 or args.dist:
         from paper_2204_06666_b200 import distributed as D
 
-        return D.bench_main(args)
+        return D.bench_main(args, ClockSampler)
 
     dev = 0
     torch.cuda.set_device(dev)
@@ -313,6 +313,33 @@ def run_gpu(args):
     value = flops / t_step / 1e9
     achieved = bmin / t_step / 1e9
     peak, peak_src = measured_peak()
+
+    # the other arithmetic mode on the same protocol: FMA (reassociated long
+    # rows, within 1e-12 fp64 / 1e-5 fp32 of the strict result) or strict
+    other = not args.fma
+    y_main = y.clone()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(min(args.steps, 200))]
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}") if flush_l2 else None
+    for _ in range(3):
+        dm.spmv(xr, y, fma=other, stream=stream)
+    for a, b in evs:
+        if scratch is not None:
+            with torch.cuda.stream(stream):
+                scratch.fill_(1)
+        a.record(stream)
+        dm.spmv(xr, y, fma=other, stream=stream)
+        b.record(stream)
+    stream.synchronize()
+    t_other = sum(a.elapsed_time(b) for a, b in evs) / 1e3 / len(evs)
+    del scratch
+    yo = y.cpu().numpy().astype(np.float64)
+    ym = y_main.cpu().numpy().astype(np.float64)
+    den = float(np.max(np.abs(ym))) or 1.0
+    other_mode = {"mode": "fma" if other else "strict", "avg_us": t_other * 1e6,
+                  "gflops": flops / t_other / 1e9, "effective_gbs": bmin / t_other / 1e9,
+                  "rel_err_vs_main": float(np.max(np.abs(yo - ym))) / den}
+    y.copy_(y_main)
 
     # ---- cuSPARSE CSR comparator, same protocol
     cus = {}
@@ -422,6 +449,7 @@ def run_gpu(args):
         "parity": parity,
         "cusparse": cus,
         "kernel": {"avg_us": t_step * 1e6, "effective_gbs": achieved,
+                   "mode": "fma" if args.fma else "strict", "other_mode": other_mode,
                    "l2_resident_avg_us": None if t_resident is None else t_resident * 1e6,
                    "traffic_model_bytes": E.traffic_model(e), "device_info": info},
         "preprocessing": dict(prep_t, prep_to_spmv_ratio=(prep_t["partition_s"]

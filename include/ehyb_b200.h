@@ -160,6 +160,7 @@ typedef struct ehyb_dev_info {
   int64_t pool_slices;        /* ER slices in the cross-CTA pool (0 = pool off) */
   int32_t er_buf_slices;      /* own ER slices buffered in shared memory per CTA */
   int32_t smem_bytes;         /* dynamic shared memory of a fused launch */
+  int64_t long_rows;          /* rows computed by the long-row path (width > EHYB_LONG_ROW) */
 } ehyb_dev_info;
 
 /* Upload an assembled matrix once (device = CUDA ordinal) and derive the
@@ -174,16 +175,17 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
  *                           L2 prefetch (0 = off)
  *   EHYB_TUNE_PREFETCH_ER   1 = bulk-prefetch each warp's next ER slice
  *   EHYB_TUNE_THREADS       threads per CTA (multiple of 32, <= 1024)
- *   EHYB_TUNE_TIMING        device pointer to n_parts*4 u64 %globaltimer
+ *   EHYB_TUNE_TIMING        device pointer to n_parts*8 u64 %globaltimer
  *                           stamps per CTA (start, window ready, ELL
- *                           drained, end), 0 = off */
+ *                           issue drained, end, own ER done, combine done,
+ *                           pool done, ELL published), zeroed by the
+ *                           caller, 0 = off */
 #define EHYB_TUNE_PREFETCH_ELL 1
 #define EHYB_TUNE_PREFETCH_ER 2
 #define EHYB_TUNE_THREADS 3
 #define EHYB_TUNE_TIMING 4
 #define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 4) */
 #define EHYB_TUNE_CLAIM_AHEAD 6 /* bit0: ELL chunks, bit1: ER slices claimed one ahead */
-#define EHYB_TUNE_ER_MIX 7 /* 1 = buffered own ER slices interleaved with ELL chunks */
 EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value);
 
 /* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].

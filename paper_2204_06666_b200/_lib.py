@@ -21,7 +21,6 @@ EINVAL, ENOMEM, ECUDA = 1, 2, 3
 MODE_STRICT, MODE_FMA = 0, 1
 TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING, TUNE_ER_WARPS = 1, 2, 3, 4, 5
 TUNE_CLAIM_AHEAD = 6
-TUNE_ER_MIX = 7
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -62,6 +61,7 @@ class DevInfo(C.Structure):
         ("window_bytes", C.c_int64), ("window_in_smem", C.c_int32),
         ("threads_per_cta", C.c_int32), ("ctas", C.c_int32), ("sm_count", C.c_int32),
         ("pool_slices", C.c_int64), ("er_buf_slices", C.c_int32), ("smem_bytes", C.c_int32),
+        ("long_rows", C.c_int64),
     ]
 
 

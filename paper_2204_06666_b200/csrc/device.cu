@@ -105,18 +105,36 @@ struct ehyb_dev {
   size_t win_bytes = 0;  // window part
   bool window_in_smem = false, window_tma = false;
   int sm_count = 0;
+  int64_t max_ctas = 1;  // co-resident CTAs of the fused kernel (occupancy x SMs)
   size_t bytes = 0;
   // tuning knobs (ehyb_dev_tune) and optional per-CTA timing buffer
   int pf_ell = 0, pf_er = 1;
   unsigned long long* timing = nullptr;
   // ER pool (cross-CTA load balance)
   int64_t pool_lo = 0, pool_hi = 0;
-  unsigned int* part_flag = nullptr;
+  unsigned int* pool_done = nullptr;
+  int32_t* pool_own_ptr = nullptr;
+  int32_t* pool_own_idx = nullptr;
+  void* pool_acc = nullptr;
   unsigned int* pool_ctr = nullptr;
   unsigned int epoch = 0;
   // own-ER shared-memory buffer
   int er_buf_slices = 0, er_buf_offset = 0, er_warps = 4;
-  int ell_ahead = 0, er_ahead = 0, er_mix = 0;
+  int ell_ahead = 1, er_ahead = 1;
+  // long rows (derived): masked out of the slice paths, computed by warps
+  uint32_t* long_bits = nullptr;
+  int32_t lr_tasks = 0, lr_segs = 0;
+  int64_t* lr_span = nullptr;
+  int32_t* lr_row = nullptr;
+  int64_t* lr_padcol = nullptr;
+  void* lr_val = nullptr;
+  uint32_t* lr_col = nullptr;
+  int64_t* lr_seg = nullptr;
+  int32_t* lr_task_seg = nullptr;
+  int32_t* lr_task_nell = nullptr;
+  void* lr_part = nullptr;
+  unsigned int* lr_cnt = nullptr;
+  unsigned int* lr_ctr = nullptr;
   // host-batch pipeline (ehyb_dev_spmv_host_many): copy-in / copy-out streams,
   // two device buffer pairs, per-buffer events
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -128,7 +146,9 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    part_flag, pool_ctr, bx[0], bx[1], by[0], by[1]};
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, bx[0], bx[1], by[0], by[1], long_bits, lr_span,
+                    lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
+                    lr_part, lr_cnt, lr_ctr};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (int b = 0; b < 2; ++b) {
@@ -172,14 +192,31 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_lo = h->pool_lo;
   P.pool_hi = h->pool_hi;
   P.pool_ctr = h->pool_ctr;
-  P.part_flag = h->part_flag;
+  P.pool_done = h->pool_done;
+  P.pool_own_ptr = h->pool_own_ptr;
+  P.pool_own_idx = h->pool_own_idx;
+  P.pool_acc = static_cast<T*>(h->pool_acc);
   P.epoch = h->epoch;
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
   P.er_warps = h->er_warps;
+  P.n_parts = int32_t(h->local_rows / h->vec);
   P.ell_ahead = h->ell_ahead;
   P.er_ahead = h->er_ahead;
-  P.er_mix = h->er_mix;
+  P.long_bits = h->long_bits;
+  P.lr_tasks = h->lr_tasks;
+  P.lr_span = h->lr_span;
+  P.lr_row = h->lr_row;
+  P.lr_padcol = h->lr_padcol;
+  P.lr_val = static_cast<const T*>(h->lr_val);
+  P.lr_col = h->lr_col;
+  P.lr_segs = h->lr_segs;
+  P.lr_seg = h->lr_seg;
+  P.lr_task_seg = h->lr_task_seg;
+  P.lr_task_nell = h->lr_task_nell;
+  P.lr_part = static_cast<T*>(h->lr_part);
+  P.lr_cnt = h->lr_cnt;
+  P.lr_ctr = h->lr_ctr;
   auto kern = (do_ell && h->window_in_smem) ? spmv_fused_kernel<T, STRICT, C32, true>
                               : spmv_fused_kernel<T, STRICT, C32, false>;
   // dynamic smem: [window | own-ER buffer]; the buffer is only used when one
@@ -187,7 +224,6 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   const size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
   if (!(do_ell && do_er)) {
     P.er_buf_slices = 0;
-    P.er_mix = 0;
   }
   if (smem > 48 * 1024) {
     // opt in once per (kernel, device) to the largest window any handle needs
@@ -203,8 +239,10 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
       configured[key] = smem;
     }
   }
+  // at most one wave of resident CTAs; each loops over its partitions
   const int64_t n_local_parts = h->local_rows / h->vec;
-  kern<<<dim3(unsigned(n_local_parts)), dim3(unsigned(h->threads)), smem, st>>>(P);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(n_local_parts, h->max_ctas));
+  kern<<<dim3(unsigned(grid)), dim3(unsigned(h->threads)), smem, st>>>(P);
   return cudaGetLastError();
 }
 
@@ -221,7 +259,7 @@ cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, boo
 
 cudaError_t launch_spmv(ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
                         cudaStream_t st) {
-  if (ell) h->epoch += 1;  // the ER-only launch of a split SpMV reuses its ELL epoch
+  h->epoch += 1;  // per-launch counters alternate by epoch parity
   return h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
                      : launch_mode<double>(h, x, y, mode, ell, er, st);
 }
@@ -294,17 +332,56 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::vector<int32_t> pos(size_t(s_hi - s_lo) + 1);
   for (int64_t s = s_lo; s <= s_hi; ++s) pos[size_t(s - s_lo)] = int32_t(m->position_ell[s] - base);
   CUDA_TRY(upload(&h->pos_ell, pos.data(), pos.size() * 4, &h->bytes));
-  CUDA_TRY(upload(&h->width_ell, m->width_ell + s_lo, size_t(s_hi - s_lo) * 4, &h->bytes));
   CUDA_TRY(upload(&h->val_ell, static_cast<const char*>(m->val_ell) + size_t(base) * tb,
                   size_t(slots) * tb, &h->bytes));
   CUDA_TRY(upload(&h->col_ell, m->col_ell + base, size_t(slots) * 2, &h->bytes));
+
+  // ---- long rows: ELL or ER width above the threshold. They leave the slice
+  // paths (lane masked, slice narrowed to its widest remaining lane) and are
+  // computed whole by warps (include/ehyb_b200.h, "long rows").
+  const int64_t long_w = std::max<int64_t>(1, int64_t(env_double("EHYB_LONG_ROW", 128.0)));
+  std::vector<int64_t> long_rows;
+  std::unordered_map<int64_t, int64_t> long_er;  // row -> ER row j
+  for (int64_t r = row_lo; r < row_hi; ++r)
+    if (m->ell_row_widths[r] > long_w) long_rows.push_back(r);
+  for (int64_t j = 0; j < m->n_er_rows; ++j) {
+    const int64_t r = m->y_idx_er[j];
+    if (r < row_lo || r >= row_hi) continue;
+    if (m->er_row_widths[j] > long_w || m->ell_row_widths[r] > long_w) {
+      if (m->er_row_widths[j] > long_w && m->ell_row_widths[r] <= long_w) long_rows.push_back(r);
+      long_er[r] = j;
+    }
+  }
+  std::sort(long_rows.begin(), long_rows.end());
+  std::vector<uint32_t> lbits(size_t((h->local_rows + 31) / 32) + 1, 0u);
+  for (int64_t r : long_rows) lbits[size_t((r - row_lo) >> 5)] |= 1u << ((r - row_lo) & 31);
+  {
+    std::vector<int32_t> eff(size_t(s_hi - s_lo));
+    for (int64_t s = s_lo; s < s_hi; ++s) {
+      const int32_t W = m->width_ell[s];
+      int32_t wmax = 0;
+      bool has_long = false;
+      for (int64_t r = s * C; r < (s + 1) * C; ++r) {
+        const int64_t lr = r - row_lo;
+        if ((lbits[size_t(lr >> 5)] >> (lr & 31)) & 1u) has_long = true;
+        else wmax = std::max<int32_t>(wmax, m->ell_row_widths[r]);
+      }
+      int32_t e = has_long ? wmax : W;
+      if (e > kEffWidth) return fail("ELL slice width exceeds the device limit");
+      if (has_long) e |= kEffHasLong | (wmax < W ? kEffPadTail : 0);
+      eff[size_t(s - s_lo)] = e;
+    }
+    CUDA_TRY(upload(&h->width_ell, eff.data(), eff.size() * 4, &h->bytes));
+  }
+  CUDA_TRY(upload(&h->long_bits, lbits.data(), lbits.size() * 4, &h->bytes));
 
   // ---- ER regrouped per owning partition
   const int64_t n_loc_parts = p1 - p0;
   std::vector<std::vector<int64_t>> members(static_cast<size_t>(n_loc_parts));
   for (int64_t j = 0; j < m->n_er_rows; ++j) {
     const int64_t r = m->y_idx_er[j];
-    if (r >= row_lo && r < row_hi) members[size_t(r / vec - p0)].push_back(j);
+    if (r >= row_lo && r < row_hi && !((lbits[size_t((r - row_lo) >> 5)] >> ((r - row_lo) & 31)) & 1u))
+      members[size_t(r / vec - p0)].push_back(j);
   }
   std::unordered_map<int64_t, int64_t> halo_index;
   halo_index.reserve(size_t(n_halo) * 2 + 1);
@@ -328,7 +405,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(32, chunks * 32)));
   int per_sm = 0;
   CUDA_TRY(occupancy(h.get(), &per_sm));
-  const bool pool_ok = n_loc_parts <= int64_t(per_sm) * h->sm_count;
+  h->max_ctas = std::max<int64_t>(1, int64_t(per_sm) * h->sm_count);
+  // the launch never exceeds one resident wave, so pooled rows (which wait on
+  // other CTAs' ELL publication) cannot deadlock
+  const bool pool_ok = true;
 
   // per-partition 32-row ER slices (members in reference order), then the
   // own / pool split: partition q keeps the prefix of its ER slices that fits
@@ -444,6 +524,94 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   CUDA_TRY(upload(&h->er_val, evals.data(), size_t(eslots) * tb, &h->bytes));
   CUDA_TRY(upload(&h->er_col, ecols.data(), size_t(eslots) * 4, &h->bytes));
 
+  // ---- long-row tasks: entries in the reference's k order with x indices
+  // (ELL window columns made shard-local), longest first; FMA-mode segments
+  if (!long_rows.empty()) {
+    struct Task { int64_t row, n_ell, n_er; };
+    std::vector<Task> tasks;
+    for (int64_t r : long_rows) {
+      auto it = long_er.find(r);
+      tasks.push_back({r, m->ell_row_widths[r], it == long_er.end() ? 0 : m->er_row_widths[it->second]});
+    }
+    std::stable_sort(tasks.begin(), tasks.end(), [](const Task& a, const Task& b) {
+      return a.n_ell + a.n_er > b.n_ell + b.n_er;
+    });
+    const int64_t n_t = int64_t(tasks.size());
+    const int64_t seg_len = std::max<int64_t>(256, int64_t(env_double("EHYB_LONG_SEG", 4096.0)));
+    std::vector<int64_t> span(static_cast<size_t>(3 * n_t)), padcol(static_cast<size_t>(n_t)), seg;
+    std::vector<int32_t> lrow(static_cast<size_t>(n_t)), tseg(static_cast<size_t>(n_t) + 1, 0),
+        tnell(static_cast<size_t>(n_t), 0);
+    int64_t total = 0;
+    for (const auto& t : tasks) total += t.n_ell + t.n_er;
+    std::vector<char> lval(size_t(std::max<int64_t>(total, 1)) * tb, 0);
+    std::vector<uint32_t> lcol(size_t(std::max<int64_t>(total, 1)), 0);
+    int64_t at = 0;
+    for (int64_t i = 0; i < n_t; ++i) {
+      const auto& t = tasks[size_t(i)];
+      const int64_t r = t.row, s = r / C, lane = r % C;
+      const int64_t win0 = (r / vec) * vec - row_lo;  // shard-local index of window column 0
+      span[size_t(3 * i)] = at;
+      for (int64_t k = 0; k < t.n_ell; ++k, ++at) {
+        const int64_t src = int64_t(m->position_ell[s]) + lane + C * k;
+        std::memcpy(&lval[size_t(at) * tb], static_cast<const char*>(m->val_ell) + size_t(src) * tb, tb);
+        lcol[size_t(at)] = uint32_t(win0 + m->col_ell[src]);
+      }
+      span[size_t(3 * i + 1)] = at;
+      int32_t flags = 0;
+      if (t.n_ell < m->width_ell[s]) flags |= kLrEllPad;
+      padcol[size_t(i)] = win0;
+      if (auto it = long_er.find(r); it != long_er.end()) {
+        const int64_t j = it->second;
+        flags |= kLrHasEr;
+        if (!shard && t.n_er < m->width_er[j / C]) flags |= kLrErPad;
+        const int64_t src0 = int64_t(m->position_er[j / C]) + j % C;
+        for (int64_t k = 0; k < t.n_er; ++k, ++at) {
+          const int64_t src = src0 + C * k;
+          std::memcpy(&lval[size_t(at) * tb], static_cast<const char*>(m->val_er) + size_t(src) * tb, tb);
+          const int64_t c = m->col_er[src];
+          int64_t lc;
+          if (c >= row_lo && c < row_hi) {
+            lc = c - row_lo;
+          } else {
+            auto hit = halo_index.find(c);
+            if (hit == halo_index.end()) return fail("ER column missing from the shard halo plan");
+            lc = hit->second;
+          }
+          lcol[size_t(at)] = uint32_t(lc);
+        }
+      }
+      span[size_t(3 * i + 2)] = at;
+      lrow[size_t(i)] = int32_t(r - row_lo) | flags;
+      tseg[size_t(i)] = int32_t(seg.size() / 3);
+      for (int part_i = 0; part_i < 2; ++part_i) {
+        const int64_t lo = span[size_t(3 * i + part_i)], hi = span[size_t(3 * i + part_i + 1)];
+        for (int64_t a = lo; a < hi; a += seg_len) {
+          seg.push_back(i);
+          seg.push_back(a);
+          seg.push_back(std::min(hi, a + seg_len));
+          if (part_i == 0) tnell[size_t(i)] += 1;
+        }
+      }
+    }
+    tseg[size_t(n_t)] = int32_t(seg.size() / 3);
+    h->lr_tasks = int32_t(n_t);
+    h->lr_segs = int32_t(seg.size() / 3);
+    CUDA_TRY(upload(&h->lr_span, span.data(), span.size() * 8, &h->bytes));
+    CUDA_TRY(upload(&h->lr_row, lrow.data(), lrow.size() * 4, &h->bytes));
+    CUDA_TRY(upload(&h->lr_padcol, padcol.data(), padcol.size() * 8, &h->bytes));
+    CUDA_TRY(upload(&h->lr_val, lval.data(), size_t(total) * tb, &h->bytes));
+    CUDA_TRY(upload(&h->lr_col, lcol.data(), size_t(total) * 4, &h->bytes));
+    CUDA_TRY(upload(&h->lr_seg, seg.data(), seg.size() * 8, &h->bytes));
+    CUDA_TRY(upload(&h->lr_task_seg, tseg.data(), tseg.size() * 4, &h->bytes));
+    CUDA_TRY(upload(&h->lr_task_nell, tnell.data(), tnell.size() * 4, &h->bytes));
+    CUDA_TRY(cudaMalloc(&h->lr_part, size_t(std::max<int32_t>(h->lr_segs, 1)) * tb));
+    CUDA_TRY(cudaMalloc(&h->lr_cnt, size_t(n_t) * 4));
+    CUDA_TRY(cudaMemset(h->lr_cnt, 0, size_t(n_t) * 4));
+    CUDA_TRY(cudaMalloc(&h->lr_ctr, 16));
+    CUDA_TRY(cudaMemset(h->lr_ctr, 0, 16));
+    h->bytes += size_t(std::max<int32_t>(h->lr_segs, 1)) * tb + size_t(n_t) * 4 + 16;
+  }
+
   // ---- permutation tables (int32) for the user-order entry points
   if (!shard) {
     std::vector<int32_t> ro(static_cast<size_t>(m->dimension)), inv(static_cast<size_t>(padded));
@@ -453,13 +621,24 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(upload(&h->inverse, inv.data(), inv.size() * 4, &h->bytes));
   }
 
-  // ---- ER pool state: claim counters and per-partition publication epochs
+  // ---- ER pool state: claim counters, per-owner lists, scratch, counts
   if (h->pool_hi > h->pool_lo) {
-    CUDA_TRY(cudaMalloc(&h->part_flag, size_t(n_loc_parts) * 4 + 16));
-    CUDA_TRY(cudaMemset(h->part_flag, 0, size_t(n_loc_parts) * 4 + 16));
+    std::vector<int32_t> optr(static_cast<size_t>(n_loc_parts) + 1, 0), oidx;
+    for (int64_t sl = h->pool_lo; sl < h->pool_hi; ++sl) optr[size_t(order[size_t(sl)].q) + 1] += 1;
+    for (int64_t q = 0; q < n_loc_parts; ++q) optr[size_t(q) + 1] += optr[size_t(q)];
+    oidx.resize(size_t(h->pool_hi - h->pool_lo));
+    std::vector<int32_t> fill(optr.begin(), optr.end() - 1);
+    for (int64_t sl = h->pool_lo; sl < h->pool_hi; ++sl)
+      oidx[size_t(fill[size_t(order[size_t(sl)].q)]++)] = int32_t(sl);
+    CUDA_TRY(upload(&h->pool_own_ptr, optr.data(), optr.size() * 4, &h->bytes));
+    CUDA_TRY(upload(&h->pool_own_idx, oidx.data(), oidx.size() * 4, &h->bytes));
+    const size_t acc_bytes = size_t(h->pool_hi - h->pool_lo) * 32 * tb;
+    CUDA_TRY(cudaMalloc(&h->pool_acc, acc_bytes));
+    CUDA_TRY(cudaMalloc(&h->pool_done, size_t(n_loc_parts) * 8 + 16));
+    CUDA_TRY(cudaMemset(h->pool_done, 0, size_t(n_loc_parts) * 8 + 16));
     CUDA_TRY(cudaMalloc(&h->pool_ctr, 16));
     CUDA_TRY(cudaMemset(h->pool_ctr, 0, 16));
-    h->bytes += size_t(n_loc_parts) * 4 + 32;
+    h->bytes += acc_bytes + size_t(n_loc_parts) * 8 + 32;
   }
   *out = h.release();
   return 0;
@@ -510,7 +689,6 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
       h->ell_ahead = int(value & 1);
       h->er_ahead = int((value >> 1) & 1);
       return 0;
-    case EHYB_TUNE_ER_MIX: h->er_mix = value ? 1 : 0; return 0;
     case EHYB_TUNE_TIMING:
       h->timing = reinterpret_cast<unsigned long long*>(static_cast<uintptr_t>(value));
       return 0;
@@ -527,11 +705,12 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out) {
   out->window_bytes = h->vec * h->tau;
   out->window_in_smem = h->window_in_smem ? 1 : 0;
   out->threads_per_cta = h->threads;
-  out->ctas = int32_t(h->local_rows / h->vec);
+  out->ctas = int32_t(std::min<int64_t>(h->local_rows / h->vec, h->max_ctas));
   out->sm_count = h->sm_count;
   out->pool_slices = h->pool_hi - h->pool_lo;
   out->er_buf_slices = h->er_buf_slices;
   out->smem_bytes = int32_t(h->smem);
+  out->long_rows = h->lr_tasks;
   return 0;
 }
 

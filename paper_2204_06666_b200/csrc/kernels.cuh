@@ -55,20 +55,53 @@ struct SpmvParams {
   int32_t do_er;
   int32_t pf_ell;            // ELL slices kept in flight ahead of the warps by L2 bulk prefetch (0 = off)
   int32_t pf_er;             // 1 = L2 bulk prefetch of the next ER slice per warp
-  unsigned long long* timing;  // optional per-CTA %globaltimer stamps [start, window, ell, end]
-  // ER work pool shared by all CTAs (load balance across partitions)
+  unsigned long long* timing;  // optional per-CTA %globaltimer stamps [start, window, ell issue
+                               // end, end, own ER, combine, pool, ell published] (8 per CTA)
+  // ER work pool shared by all CTAs (load balance across partitions): any
+  // warp computes pooled slices into a global scratch at any time; the
+  // owning CTA adds them to its rows once all of them are in
   int64_t pool_lo, pool_hi;         // global slice range of the pool
   unsigned int* pool_ctr;           // [2] claim counters, alternating by epoch
-  unsigned int* part_flag;          // [n_parts] epoch whose ELL phase the partition published
+  unsigned int* pool_done;          // [2][n_parts] computed pooled slices per owner, by epoch
+  const int32_t* __restrict__ pool_own_ptr;  // [n_parts+1] pooled slices of each partition
+  const int32_t* __restrict__ pool_own_idx;  // their slice indices
+  T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
   unsigned int epoch;               // launch sequence number (>= 1)
   // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
   int32_t er_buf_slices;            // buffered own ER slices (<= kMaxErBuf)
   int32_t er_buf_offset;            // byte offset of the buffer in dynamic smem
   int32_t er_warps;                 // warps that start on ER before ELL
+  int32_t n_parts;                  // partitions of this launch (grid may be smaller: CTAs loop)
   int32_t ell_ahead;                // 1 = claim the next ELL chunk (and its metadata) one ahead
   int32_t er_ahead;                 // 1 = same for ER slices
-  int32_t er_mix;                   // 1 = own buffered ER slices interleaved with ELL chunks
+  // long rows (derived at upload): rows whose ELL or ER width exceeds the long
+  // threshold leave the slice paths (their lanes are masked) and are computed
+  // by whole warps claimed at kernel start
+  const uint32_t* __restrict__ long_bits;  // [local_rows/32] bit per masked row
+  int32_t lr_tasks;                        // long rows
+  const int64_t* __restrict__ lr_span;     // [3*tasks] lo, mid (ELL|ER split), hi
+  const int32_t* __restrict__ lr_row;      // [tasks] row | kLrEllPad | kLrErPad | kLrHasEr
+  const int64_t* __restrict__ lr_padcol;   // [tasks] x index of the ELL padding product
+  const T* __restrict__ lr_val;
+  const uint32_t* __restrict__ lr_col;     // x indices (window columns made global)
+  int32_t lr_segs;                         // FMA mode: segments of the long rows
+  const int64_t* __restrict__ lr_seg;      // [3*segs] task, lo, hi
+  const int32_t* __restrict__ lr_task_seg; // [tasks+1] segment range of each task
+  const int32_t* __restrict__ lr_task_nell;// [tasks] ELL segments of each task
+  T* __restrict__ lr_part;                 // [segs] segment partial sums
+  unsigned int* lr_cnt;                    // [tasks] finished segments (self-resetting)
+  unsigned int* lr_ctr;                    // [2] task / segment claim counters by epoch
 };
+
+// ell_eff (the slice widths the kernel reads) = effective width | flags
+constexpr int32_t kEffWidth = 0x00ffffff;
+constexpr int32_t kEffPadTail = 1 << 29;  // lanes owe the reference's padding products 0*win[0]
+constexpr int32_t kEffHasLong = 1 << 30;  // a lane of the slice is a long row (long_bits)
+// lr_row flags
+constexpr int32_t kLrRowMask = 0x0fffffff;
+constexpr int32_t kLrEllPad = 1 << 28;
+constexpr int32_t kLrErPad = 1 << 29;
+constexpr int32_t kLrHasEr = 1 << 30;
 
 constexpr int32_t kPadFlag = 0x40000000;  // row had reference ER padding slots
 constexpr int32_t kRowMask = 0x3fffffff;
@@ -164,10 +197,10 @@ struct EllUnroll {
   static constexpr int value = sizeof(T) == 4 ? 16 : 8;
 };
 
-template <typename T, bool STRICT>
+template <typename T, bool STRICT, bool WAIT>
 __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
                                          const uint16_t* __restrict__ col, int64_t pos, int w,
-                                         const T* win, uint64_t* win_bar) {
+                                         const T* win, uint64_t* win_bar, uint32_t win_phase) {
   constexpr int U = EllUnroll<T>::value;
   T acc = T(0);
   int k = 0;
@@ -180,9 +213,8 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
     for (int u = 0; u < U; ++u) v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
     // a warp's first chunk issues its stream loads before the window has
     // landed: the TMA copy and the first HBM round trip overlap
-    if (win_bar) {
-      mbar_wait(win_bar, 0);
-      win_bar = nullptr;
+    if constexpr (WAIT) {
+      if (k == 0) mbar_wait(win_bar, win_phase);
     }
     T xv[U];
 #pragma unroll
@@ -202,7 +234,9 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
         v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
       }
     }
-    if (win_bar) mbar_wait(win_bar, 0);
+    if constexpr (WAIT) {
+      if (k == 0) mbar_wait(win_bar, win_phase);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (k + u < w) acc = madd<STRICT>(acc, v[u], win[c[u]]);
@@ -255,6 +289,22 @@ __device__ __forceinline__ ErMeta er_slice_meta(const SpmvParams<T>& P, int64_t 
   return m;
 }
 
+// Metadata of a claimed ER slice (s >= s_end: an empty claim) plus a precise
+// L2 bulk prefetch of its values and columns.
+template <typename T>
+__device__ __forceinline__ ErMeta er_claimed_meta(const SpmvParams<T>& P, int64_t s,
+                                                  int64_t s_end, int lane) {
+  ErMeta m{-1, 0, 0, 0};
+  if (s < s_end) {
+    m = er_slice_meta(P, s, lane);
+    if (lane == 0 && P.pf_er && m.sw > 0) {
+      bulk_prefetch_l2(P.er_val + m.pos - lane, uint32_t(32 * int64_t(m.sw) * int64_t(sizeof(T))));
+      bulk_prefetch_l2(P.er_col + m.pos - lane, uint32_t(32 * int64_t(m.sw) * 4));
+    }
+  }
+  return m;
+}
+
 // Products of one ER row in k order, x through the read-only path; the
 // reference's ER padding products 0*x[0] (engine.py:148-151) are inert for
 // finite x and NaN-propagating otherwise — reproduced with one product.
@@ -284,6 +334,195 @@ __device__ __forceinline__ T er_slice_compute(const SpmvParams<T>& P, const ErMe
   return acc;
 }
 
+// ------------------------------------------------------------- long rows
+// STRICT: the reference's serial order over entries [lo, hi) — acc from +0.0,
+// each product rounded, then added. Entries are fetched 32*LB at a time (lane
+// i holds entry base+i) two blocks ahead behind an L2 bulk prefetch, their x
+// gathered one block ahead, and the rounded products staged in shared memory
+// so the only exposed latency is the dependent add chain itself.
+template <typename T>
+__device__ __forceinline__ T long_chain_strict(const SpmvParams<T>& P, int64_t lo, int64_t hi,
+                                               int lane, T* stage) {
+  constexpr int LB = 2;
+  constexpr int BLK = 32 * LB;
+  T acc = T(0);
+  if (hi <= lo) return acc;
+  auto load = [&](int64_t base, T* v, uint32_t* c) {
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int64_t i = base + 32 * b + lane;
+      c[b] = 0;
+      v[b] = T(0);
+      if (i < hi) {
+        c[b] = __ldcs(P.lr_col + i);
+        v[b] = __ldcs(P.lr_val + i);
+      }
+    }
+  };
+  T v1[LB], v2[LB], x1[LB];
+  uint32_t c1[LB], c2[LB];
+  load(lo, v1, c1);
+  load(lo + BLK, v2, c2);
+#pragma unroll
+  for (int b = 0; b < LB; ++b) x1[b] = (lo + 32 * b + lane < hi) ? __ldg(P.x + c1[b]) : T(0);
+  for (int64_t base = lo; base < hi; base += BLK) {
+    if (lane == 0) {  // keep the entry stream in L2 well ahead of the loads
+      const int64_t a = (base + 16 * BLK) & ~int64_t(3);
+      const int64_t n = (hi - a < 4 * BLK ? hi - a : 4 * BLK) & ~int64_t(3);
+      if (n > 0) {
+        bulk_prefetch_l2(P.lr_val + a, uint32_t(n * int64_t(sizeof(T))));
+        bulk_prefetch_l2(P.lr_col + a, uint32_t(n * 4));
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < LB; ++b) stage[32 * b + lane] = mul_rn(v1[b], x1[b]);
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      v1[b] = v2[b];
+      c1[b] = c2[b];
+    }
+    load(base + 2 * BLK, v2, c2);
+#pragma unroll
+    for (int b = 0; b < LB; ++b)
+      x1[b] = (base + BLK + 32 * b + lane < hi) ? __ldg(P.x + c1[b]) : T(0);
+    const int64_t rem = hi - base;
+    if (rem >= BLK) {
+#pragma unroll
+      for (int i = 0; i < BLK; ++i) acc = add_rn(acc, stage[i]);
+    } else {
+      for (int i = 0; i < int(rem); ++i) acc = add_rn(acc, stage[i]);
+    }
+  }
+  return acc;
+}
+
+// FMA mode: one segment [lo, hi) of a long row, lane-strided fused
+// multiply-adds and a fixed shuffle tree (deterministic, reassociated).
+template <typename T>
+__device__ __forceinline__ T long_segment_fast(const SpmvParams<T>& P, int64_t lo, int64_t hi,
+                                               int lane) {
+  T acc = T(0);
+  for (int64_t base = lo; base < hi; base += 32 * kUnroll) {
+    T v[kUnroll];
+    uint32_t c[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = base + 32 * u + lane;
+      c[u] = 0;
+      v[u] = T(0);
+      if (i < hi) {
+        c[u] = __ldcs(P.lr_col + i);
+        v[u] = __ldcs(P.lr_val + i);
+      }
+    }
+    T xv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) xv[u] = (base + 32 * u + lane < hi) ? __ldg(P.x + c[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (base + 32 * u + lane < hi) acc = fma(v[u], xv[u], acc);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// y of a long row from its ELL and ER accumulators (engine.py:140-154 order:
+// y = acc_ell (+ padding products); y += acc_er (+ padding products)).
+template <typename T>
+__device__ __forceinline__ T long_finish(const SpmvParams<T>& P, int task, T ell, T er) {
+  const int32_t rw = __ldg(P.lr_row + task);
+  if (rw & kLrEllPad) ell = add_rn(ell, mul_rn(T(0), __ldg(P.x + __ldg(P.lr_padcol + task))));
+  if (!(rw & kLrHasEr)) return ell;
+  if (rw & kLrErPad) er = add_rn(er, mul_rn(T(0), __ldg(P.x)));
+  return add_rn(ell, er);
+}
+
+// Long-row work of one warp, claimed from a grid-wide counter: whole rows in
+// STRICT mode (serial chains, longest first), segments in FMA mode (the last
+// segment of a row to finish sums the partials in segment order).
+template <typename T, bool STRICT>
+__device__ void long_rows_warp(const SpmvParams<T>& P, int lane, T* stage) {
+  unsigned int* ctr = P.lr_ctr + (P.epoch & 1u);
+  const int n_items = STRICT ? P.lr_tasks : P.lr_segs;
+  for (;;) {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1u);
+    const int item = int(__shfl_sync(0xffffffffu, v, 0));
+    if (item >= n_items) break;
+    if constexpr (STRICT) {
+      const int64_t lo = __ldg(P.lr_span + 3 * item), mid = __ldg(P.lr_span + 3 * item + 1),
+                    hi = __ldg(P.lr_span + 3 * item + 2);
+      const T ell = long_chain_strict(P, lo, mid, lane, stage);
+      const T er = long_chain_strict(P, mid, hi, lane, stage);
+      const T yv = long_finish(P, item, ell, er);
+      if (lane == 0) P.y[__ldg(P.lr_row + item) & kLrRowMask] = yv;
+    } else {
+      const int task = int(__ldg(P.lr_seg + 3 * item));
+      const T part = long_segment_fast(P, __ldg(P.lr_seg + 3 * item + 1),
+                                       __ldg(P.lr_seg + 3 * item + 2), lane);
+      if (lane == 0) {
+        P.lr_part[item] = part;
+        __threadfence();
+        const int s0 = __ldg(P.lr_task_seg + task), s1 = __ldg(P.lr_task_seg + task + 1);
+        if (atomicAdd(P.lr_cnt + task, 1u) == unsigned(s1 - s0 - 1)) {
+          __threadfence();
+          const int s_mid = s0 + __ldg(P.lr_task_nell + task);
+          T ell = T(0), er = T(0);
+          for (int s = s0; s < s_mid; ++s) ell += __ldcg(P.lr_part + s);
+          for (int s = s_mid; s < s1; ++s) er += __ldcg(P.lr_part + s);
+          P.y[__ldg(P.lr_row + task) & kLrRowMask] = long_finish(P, task, ell, er);
+          P.lr_cnt[task] = 0u;  // ready for the next launch
+        }
+      }
+    }
+  }
+}
+
+// Pooled ER slices: claim from the grid-wide counter, compute, write the 32
+// row sums to the scratch, then count the slice for its owning partition
+// (release: the sums are visible before the count). At most `max_items`
+// slices (<= 0: until the pool is exhausted); returns false once exhausted.
+template <typename T, bool STRICT>
+__device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items) {
+  if (P.pool_hi <= P.pool_lo) return false;
+  unsigned int* ctr = P.pool_ctr + (P.epoch & 1u);
+  unsigned int* done = P.pool_done + (P.epoch & 1u) * uint32_t(P.n_parts);
+  auto pclaim = [&]() -> int64_t {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1u);
+    return P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
+  };
+  auto finish = [&](int64_t s, const ErMeta& m) {
+    const T acc = er_slice_compute<T, STRICT>(P, m);
+    P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc;
+    __threadfence();
+    __syncwarp();
+    const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
+    if (lane == 0) atomicAdd(done + uint32_t(rw0 & kRowMask) / uint32_t(P.vec), 1u);
+  };
+  if (max_items > 0) {
+    for (int i = 0; i < max_items; ++i) {
+      const int64_t s = pclaim();
+      if (s >= P.pool_hi) return false;
+      finish(s, er_claimed_meta(P, s, P.pool_hi, lane));
+    }
+    return true;
+  }
+  int64_t s = pclaim();
+  ErMeta m = er_claimed_meta(P, s, P.pool_hi, lane);
+  while (s < P.pool_hi) {  // next slice's metadata one claim ahead
+    const int64_t nxt = pclaim();
+    const ErMeta mn = er_claimed_meta(P, nxt, P.pool_hi, lane);
+    finish(s, m);
+    s = nxt;
+    m = mn;
+  }
+  return false;
+}
+
 __device__ __forceinline__ int lds_volatile(const uint32_t* p, uint32_t bit) {
   return (*reinterpret_cast<const volatile uint32_t*>(p) & bit) != 0;
 }
@@ -305,47 +544,61 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   __shared__ int next_chunk;
   __shared__ int next_er;
   __shared__ int next_comb;
+  __shared__ int next_pcomb;
   __shared__ int ell_finished;
   __shared__ uint32_t chunk_done[kMaxChunks / 32];
   __shared__ uint32_t er_done[kMaxErBuf / 32];
+  __shared__ T lr_stage[64];  // long-row products (warp 0)
 
-  const int part = blockIdx.x;
-  const int64_t row0 = int64_t(part) * P.vec;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
+  const int cta = blockIdx.x;
   const int64_t n_chunks = (P.vec + 31) >> 5;
   T* xs = reinterpret_cast<T*>(smem_raw);
-  const T* xwin = P.x + row0;
-  const int64_t s0 = __ldg(P.er_part_ptr + part);
-  const int64_t s1 = __ldg(P.er_part_ptr + part + 1);
 
   if (threadIdx.x == 0) {
-    next_chunk = 0;
-    next_er = (P.er_mix && P.do_er && P.do_ell)
-                  ? int(min(int64_t(P.er_buf_slices),
-                            int64_t(__ldg(P.er_part_ptr + part + 1) - __ldg(P.er_part_ptr + part))))
-                  : 0;
-    next_comb = 0;
-    ell_finished = 0;
-    if (P.timing) P.timing[4 * part] = globaltimer();
-    if (part == 0 && P.pool_ctr) P.pool_ctr[(P.epoch + 1u) & 1u] = 0u;  // next launch's counter
-  }
-  for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
-    chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
-  for (int i = threadIdx.x; i < kMaxErBuf / 32; i += blockDim.x) er_done[i] = 0u;
-  if constexpr (SMEM) {
-    if (P.window_tma) {
-      if (threadIdx.x == 0) {
+    if (P.timing) P.timing[8 * cta] = globaltimer();
+    if (cta == 0 && P.pool_ctr) P.pool_ctr[(P.epoch + 1u) & 1u] = 0u;  // next launch's counter
+    if (cta == 0 && P.lr_ctr) P.lr_ctr[(P.epoch + 1u) & 1u] = 0u;
+    if constexpr (SMEM) {
+      if (P.window_tma) {
         mbar_init(&bar, 1);
         fence_mbar_init();
       }
     }
   }
+
+  // Persistent over partitions: CTA b runs partitions b, b + grid, ... (one
+  // pass when the grid covers every partition). A CTA waiting for pooled
+  // slices of its partition computes pooled slices itself, and computing a
+  // pooled slice never waits, so the wait always ends.
+  for (int it = 0, part = cta; part < P.n_parts; ++it, part += gridDim.x) {
+  const int64_t row0 = int64_t(part) * P.vec;
+  const T* xwin = P.x + row0;
+  const int64_t s0 = __ldg(P.er_part_ptr + part);
+  const int64_t s1 = __ldg(P.er_part_ptr + part + 1);
+  const uint32_t phase = uint32_t(it) & 1u;
+
+  if (it > 0) __syncthreads();  // every warp is done with the previous partition
+  if (threadIdx.x == 0) {
+    next_chunk = 0;
+    next_er = 0;
+    next_comb = 0;
+    next_pcomb = 0;
+    ell_finished = 0;
+    if (P.pool_done)  // the next launch's counter of this partition
+      P.pool_done[((P.epoch + 1u) & 1u) * uint32_t(P.n_parts) + uint32_t(part)] = 0u;
+  }
+  for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
+    chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
+  for (int i = threadIdx.x; i < kMaxErBuf / 32; i += blockDim.x) er_done[i] = 0u;
   __syncthreads();
 
   if (threadIdx.x == 0) {
     if constexpr (SMEM) {
       if (P.window_tma) {
+        // the previous partition's window was read through the generic proxy
+        if (it > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint32_t bytes = uint32_t(P.vec * int64_t(sizeof(T)));
         mbar_expect_tx(&bar, bytes);
         for (uint32_t off = 0; off < bytes; off += kTmaChunk) {
@@ -372,14 +625,17 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   if constexpr (SMEM) {
     if (P.window_tma) {
       if constexpr (C32) win_pending = true;
-      else mbar_wait(&bar, 0);
+      else mbar_wait(&bar, phase);
     } else {
       for (int64_t i = threadIdx.x; i < P.vec; i += blockDim.x) xs[i] = xwin[i];
       __syncthreads();
     }
   }
   const T* win = SMEM ? xs : xwin;
-  if (P.timing && threadIdx.x == 0 && !win_pending) P.timing[4 * part + 1] = globaltimer();
+  if (P.timing && threadIdx.x == 0 && !win_pending) P.timing[8 * cta + 1] = globaltimer();
+  // long rows first (warp 0 of every CTA): their serial chains are the
+  // longest dependent work of the launch
+  if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) long_rows_warp<T, STRICT>(P, lane, lr_stage);
 
   // own ER slices [s0, s1): the first n_buf are computed into a shared-memory
   // buffer at any time (ER-first warps overlap them with the ELL stream) and
@@ -404,18 +660,19 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   // previous chunk's stream (narrow slices would otherwise pay two extra
   // round trips per chunk)
   struct EllMeta {
-    int w;
-    int64_t pos;
+    int32_t eff;  // width | kEff* flags
+    int32_t pos;
   };
   auto ell_meta = [&](int64_t chunk) -> EllMeta {
     EllMeta m{0, 0};
     if (chunk < n_chunks) {
       if constexpr (C32) {
         const int64_t s = (row0 >> 5) + chunk;
-        m.w = __ldg(P.width_ell + s);
-        m.pos = int64_t(__ldg(P.pos_ell + s));
-        if (lane == 0 && P.pf_ell > 0 && m.w > 0)  // precise L2 prefetch of the claimed chunk
-          prefetch_slice(P.val_ell, P.col_ell, m.pos, m.pos + 32 * int64_t(m.w));
+        m.eff = __ldg(P.width_ell + s);
+        m.pos = __ldg(P.pos_ell + s);
+        const int w = m.eff & kEffWidth;
+        if (lane == 0 && P.pf_ell > 0 && w > 0)  // precise L2 prefetch of the claimed chunk
+          prefetch_slice(P.val_ell, P.col_ell, int64_t(m.pos), int64_t(m.pos) + 32 * int64_t(w));
       }
     }
     return m;
@@ -434,50 +691,55 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
       // the warp publishing the partition's last chunk publishes the whole
       // ELL phase to other CTAs (pooled ER rows): one gpu-scope fence per
       // CTA instead of one per chunk
-      if (P.part_flag && atomicAdd(&ell_finished, 1) == int(n_chunks) - 1) {
-        __threadfence();
-        st_release_gpu(P.part_flag + part, P.epoch);
-      }
+      const int fin = atomicAdd(&ell_finished, 1);
+      if (P.timing && fin == int(n_chunks) - 1) P.timing[8 * cta + 7] = globaltimer();
     }
     unpublished = -1;
   };
   auto run_chunk = [&](int64_t chunk, const EllMeta& m) {
     if constexpr (C32) {
-      const T acc = ell_slice32<T, STRICT>(P.val_ell, P.col_ell, m.pos + lane, m.w, win,
-                                           (SMEM && win_pending) ? &bar : nullptr);
+      const int w = m.eff & kEffWidth;
+      T acc;
       if (SMEM && win_pending) {
+        acc = ell_slice32<T, STRICT, true>(P.val_ell, P.col_ell, int64_t(m.pos) + lane, w, win,
+                                           &bar, phase);
+        if (w == 0) mbar_wait(&bar, phase);
         win_pending = false;
-        if (P.timing && threadIdx.x == 0) P.timing[4 * part + 1] = globaltimer();
+        if (P.timing && threadIdx.x == 0) P.timing[8 * cta + 1] = globaltimer();
+      } else {
+        acc = ell_slice32<T, STRICT, false>(P.val_ell, P.col_ell, int64_t(m.pos) + lane, w, win,
+                                            nullptr, 0u);
+      }
+      bool store = true;
+      if (m.eff & (kEffPadTail | kEffHasLong)) {
+        // a slice narrowed by a long row: the reference's remaining padding
+        // products 0*win[0] (idempotent, so one stands for all of them); the
+        // long row's own lane is written by the long-row path
+        if (m.eff & kEffPadTail) acc = add_rn(acc, mul_rn(T(0), win[0]));
+        store = !((__ldg(P.long_bits + (row0 >> 5) + chunk) >> lane) & 1u);
       }
       publish();
-      P.y[row0 + chunk * 32 + lane] = acc;
+      if (store) P.y[row0 + chunk * 32 + lane] = acc;
     } else {
       const int64_t lr = chunk * 32 + lane;
       T acc = T(0);
-      if (lr < P.vec) {
+      bool skip = lr >= P.vec;
+      if (!skip) {
         const int64_t r = row0 + lr;
         const int64_t C = P.warp;
         const int64_t s = r / C;
-        const int w = __ldg(P.width_ell + s);
+        const int32_t eff = __ldg(P.width_ell + s);
         const int64_t pos = int64_t(__ldg(P.pos_ell + s)) + (r - s * C);
-        acc = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, w, C, win);
+        acc = ell_row_generic<T, STRICT>(P.val_ell, P.col_ell, pos, eff & kEffWidth, C, win);
+        if (eff & kEffPadTail) acc = add_rn(acc, mul_rn(T(0), win[0]));
+        if (eff & kEffHasLong) skip = (__ldg(P.long_bits + (r >> 5)) >> (r & 31)) & 1u;
       }
       publish();
-      if (lr < P.vec) P.y[row0 + lr] = acc;
+      if (!skip) P.y[row0 + lr] = acc;
     }
     unpublished = chunk;
   };
-  auto er_meta = [&](int64_t s, int64_t s_end) -> ErMeta {
-    ErMeta m{-1, 0, 0, 0};
-    if (s < s_end) {
-      m = er_slice_meta(P, s, lane);
-      if (lane == 0 && P.pf_er && m.sw > 0) {  // precise L2 prefetch of the claimed slice
-        bulk_prefetch_l2(P.er_val + m.pos - lane, uint32_t(32 * int64_t(m.sw) * int64_t(sizeof(T))));
-        bulk_prefetch_l2(P.er_col + m.pos - lane, uint32_t(32 * int64_t(m.sw) * 4));
-      }
-    }
-    return m;
-  };
+  auto er_meta = [&](int64_t s, int64_t s_end) { return er_claimed_meta(P, s, s_end, lane); };
   auto finish_own_er = [&](int64_t idx, const ErMeta& m) {
     const T acc = er_slice_compute<T, STRICT>(P, m);
     if (idx < n_buf) {
@@ -493,35 +755,21 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   };
 
   int64_t pending = -1;
-  const bool mix = P.er_mix && n_buf > 0;
-  if (mix) {
-    // one shared item sequence: the n_buf buffered own ER slices spread evenly
-    // among the n_chunks ELL chunks, so their gather latency hides behind the
-    // ELL stream of the other warps; item t is ER slice floor(t*n_buf/total)
-    // when that floor steps at t, else ELL chunk t - floor(t*n_buf/total)
-    const int64_t total = n_chunks + n_buf;
-    for (int64_t t = claim(&next_chunk); t < total; t = claim(&next_chunk)) {
-      const int64_t e0 = (t * n_buf) / total;
-      if (((t + 1) * n_buf) / total > e0) {
-        finish_own_er(e0, er_meta(s0 + e0, s1));
-        publish();
-      } else {
-        run_chunk(t - e0, ell_meta(t - e0));
+  if (P.do_er && P.do_ell && wid < P.er_warps) {  // ER-first warps
+    if (n_buf > 0) {
+      for (;;) {
+        const int64_t idx = claim(&next_er);
+        if (idx >= n_buf) {
+          pending = idx;
+          break;
+        }
+        finish_own_er(idx, er_meta(s0 + idx, s1));
       }
-      if (P.timing && lane == 0 && t + 1 == total) P.timing[4 * part + 2] = globaltimer();
     }
-    publish();
-  } else if (n_buf > 0 && wid < P.er_warps) {  // ER-first warps
-    for (;;) {
-      const int64_t idx = claim(&next_er);
-      if (idx >= n_buf) {
-        pending = idx;
-        break;
-      }
-      finish_own_er(idx, er_meta(s0 + idx, s1));
-    }
+    // pooled slices of every partition, hidden behind the other warps' ELL stream
+    pool_drain<T, STRICT>(P, lane, 0);
   }
-  if (P.do_ell && !mix) {
+  if (P.do_ell) {
     int64_t chunk = claim(&next_chunk);
     if (P.ell_ahead) {
       EllMeta m = ell_meta(chunk);
@@ -537,7 +785,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
     }
     publish();  // this warp's last chunk
     // the warp whose claim first ran past the end stamps the end of ELL issue
-    if (P.timing && lane == 0 && chunk == n_chunks) P.timing[4 * part + 2] = globaltimer();
+    if (P.timing && lane == 0 && chunk == n_chunks) P.timing[8 * cta + 2] = globaltimer();
   }
 
   if (P.do_er) {
@@ -556,6 +804,11 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
       for (int64_t idx = claim(&next_er); idx < n_own; idx = claim(&next_er))
         finish_own_er(idx, er_meta(s0 + idx, s1));
     }
+    auto stamp = [&](int i) {
+      if (P.timing && lane == 0) atomicMax(P.timing + 8 * cta + i, globaltimer());
+    };
+    stamp(4);
+    pool_drain<T, STRICT>(P, lane, 0);  // whatever the ER-first warps left
     // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
     for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
       while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
@@ -568,37 +821,33 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
         P.y[r] = add_rn(__ldcg(P.y + r), er_buf[idx * 32 + lane]);
       }
     }
-    // shared pool: excess ER slices of heavy partitions, claimed by any CTA;
-    // rows of other CTAs are finished once their ELL chunk is published
-    if (P.pool_hi > P.pool_lo) {
-      unsigned int* ctr = P.pool_ctr + (P.epoch & 1u);
-      auto pclaim = [&]() -> int64_t {
-        unsigned int v = 0;
-        if (lane == 0) v = atomicAdd(ctr, 1u);
-        return P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
-      };
-      int64_t s = pclaim();
-      ErMeta m = er_meta(s, P.pool_hi);
-      while (s < P.pool_hi) {
-        const int64_t nxt = pclaim();
-        const ErMeta mn = er_meta(nxt, P.pool_hi);
-        const T acc = er_slice_compute<T, STRICT>(P, m);
-        if (m.rw >= 0) {
-          const int64_t r = m.rw & kRowMask;
-          if (P.do_ell) {  // the owning CTA's ELL phase must be published
-            const uint32_t rp = uint32_t(r) / uint32_t(P.vec);
-            while (ld_acquire_gpu(P.part_flag + rp) != P.epoch) __nanosleep(64);
-          }
-          P.y[r] = add_rn(__ldcg(P.y + r), acc);
+    stamp(5);
+    // pooled slices of this partition: once all are in, y[r] = y_ell[r] + sum
+    const int32_t q0 = P.pool_own_ptr ? __ldg(P.pool_own_ptr + part) : 0;
+    const int32_t q1 = P.pool_own_ptr ? __ldg(P.pool_own_ptr + part + 1) : 0;
+    if (q1 > q0) {
+      const unsigned int* done =
+          P.pool_done + (P.epoch & 1u) * uint32_t(P.n_parts) + uint32_t(part);
+      while (ld_acquire_gpu(done) != unsigned(q1 - q0)) {
+        if (!pool_drain<T, STRICT>(P, lane, 1)) __nanosleep(128);  // help, else wait
+      }
+      for (int64_t idx = claim(&next_pcomb); idx < q1 - q0; idx = claim(&next_pcomb)) {
+        const int64_t sl = __ldg(P.pool_own_idx + q0 + idx);
+        const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
+        if (rw >= 0) {
+          const int64_t r = rw & kRowMask;
+          wait_chunk(r);
+          P.y[r] = add_rn(__ldcg(P.y + r), __ldcg(P.pool_acc + (sl - P.pool_lo) * 32 + lane));
         }
-        s = nxt;
-        m = mn;
       }
     }
+    stamp(6);
   }
+  }  // partitions of this CTA
+
   if (P.timing) {
     __syncthreads();
-    if (threadIdx.x == 0) P.timing[4 * part + 3] = globaltimer();
+    if (threadIdx.x == 0) P.timing[8 * cta + 3] = globaltimer();
   }
 }
 

@@ -69,9 +69,9 @@ class DeviceMatrix:
 
     def tune(self, *, prefetch_ell: int | None = None, prefetch_er: bool | None = None,
              threads: int | None = None, timing=False, er_warps: int | None = None,
-             claim_ahead: int | None = None, er_mix: bool | None = None) -> None:
+             claim_ahead: int | None = None) -> None:
         """Launch knobs (include/ehyb_b200.h ehyb_dev_tune). `timing`: a CUDA
-        int64 tensor of n_ctas*4 entries to record per-CTA stamps, None to
+        int64 tensor of n_ctas*8 zeroed entries to record per-CTA stamps, None to
         stop recording, False (default) to leave it unchanged."""
         if prefetch_ell is not None:
             L.call("ehyb_dev_tune", self._h, L.TUNE_PREFETCH_ELL, int(prefetch_ell))
@@ -83,8 +83,6 @@ class DeviceMatrix:
             L.call("ehyb_dev_tune", self._h, L.TUNE_ER_WARPS, int(er_warps))
         if claim_ahead is not None:
             L.call("ehyb_dev_tune", self._h, L.TUNE_CLAIM_AHEAD, int(claim_ahead))
-        if er_mix is not None:
-            L.call("ehyb_dev_tune", self._h, L.TUNE_ER_MIX, int(bool(er_mix)))
         if timing is not False:
             ptr = 0 if timing is None else int(timing.data_ptr())
             L.call("ehyb_dev_tune", self._h, L.TUNE_TIMING, ptr)

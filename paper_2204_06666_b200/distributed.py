@@ -237,6 +237,24 @@ class DistributedEhyb:
         return y_local
 
 
+    def spmv_host(self, x_local, y_local, *, fma: bool = False):
+        """Host arrays in and out (pinned for the full PCIe rate): copy the
+        owned x slice in, exchange the halo, multiply, copy the owned y out,
+        synchronise — the end-to-end call of one rank."""
+        import torch
+
+        if not hasattr(self, "_x_ext"):
+            self._x_ext = self.new_ext()
+            self._y_loc = torch.empty(self.local_rows, dtype=self.dtype,
+                                      device=f"cuda:{self.device}")
+        self._x_ext[: self.local_rows].copy_(torch.as_tensor(x_local), non_blocking=True)
+        self.spmv(self._x_ext, self._y_loc, fma=fma)
+        out = torch.as_tensor(y_local)
+        out.copy_(self._y_loc, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return y_local
+
+
 def dot(a, b, out, n: int):
     """Local fp64 dot product of the first n entries into out (device)."""
     import torch
@@ -301,7 +319,7 @@ def weak_config(world: int):
     return W.permute_symmetric(*W.stencil27(128 * world, 128, 128), seed=1)
 
 
-def bench_main(args):
+def bench_main(args, clock_cls=None):
     import json
 
     import torch
@@ -355,17 +373,40 @@ def bench_main(args):
     dist.barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    clocks = None
+    if rank == 0 and clock_cls is not None:
+        clocks = clock_cls(local)
+        clocks.__enter__()
     ev0.record()
     for _ in range(args.steps):
         A.spmv(x_ext, y)
     ev1.record()
     ev1.synchronize()
+    if clocks is not None:
+        clocks.__exit__(None, None, None)
     torch.cuda.synchronize()
     dist.barrier()
     t = torch.tensor([ev0.elapsed_time(ev1) / 1e3 / args.steps], dtype=torch.float64,
                      device=x_ext.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t)
+    # end to end: per step the owned x slice H2D (pinned), exchange + product,
+    # owned y slice D2H, synchronised; max over ranks
+    x_pin = torch.from_numpy(np.ascontiguousarray(xr[lo:hi])).pin_memory()
+    y_pin = torch.empty(A.local_rows, dtype=A.dtype).pin_memory()
+    for _ in range(3):
+        A.spmv_host(x_pin, y_pin)
+    k_e2e = max(5, min(args.steps, 100))
+    dist.barrier()
+    te0 = time.perf_counter()
+    for _ in range(k_e2e):
+        A.spmv_host(x_pin, y_pin)
+    te = torch.tensor([(time.perf_counter() - te0) / k_e2e], dtype=torch.float64,
+                      device=x_ext.device)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    t_e2e = float(te)
+    nb = torch.tensor([A.local_rows * A.dtype.itemsize], dtype=torch.int64, device=x_ext.device)
+    dist.all_reduce(nb)
     # CG: 100 iterations on b = A*1
     b = torch.empty(A.local_rows, dtype=A.dtype, device=x_ext.device)
     ones = A.new_ext()
@@ -394,6 +435,13 @@ def bench_main(args):
             "roofline": {"bound": "hbm", "achieved": bmin_total / t_step / 1e9 / world,
                          "peak": 6457.4, "unit": "GB/s (per GPU)",
                          "frac": bmin_total / t_step / 1e9 / world / 6457.4, "traffic": None},
+            "e2e": {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(nb), "d2h_bytes_per_step": int(nb),
+                    "ms_per_step": t_e2e * 1e3,
+                    "api": "DistributedEhyb.spmv_host per rank: pinned H2D of the owned x "
+                           "slice, NCCL halo exchange + fused kernels, D2H of the owned y "
+                           "slice, synchronised (max over ranks)"},
+            "clocks": clocks.summary() if clocks is not None else None,
             "halo_values_rank0": A.plan.n_halo,
             "cg": {"iterations": info["iterations"], "ms_per_iter": float(tc) / 100 * 1e3,
                    "rel_residual": info["rel_residual"]},

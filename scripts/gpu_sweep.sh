@@ -1,5 +1,9 @@
-python -c "import __graft_entry__ as g; g.build()"
-for C in cfg2 cfg3f32 cfg1; do
-timeout 900 python scripts/kernel_sweep.py --config $C --pool 0.95,0.5 --er-cost 5.0 --er-warps 4 --ahead 0,3 --pf-ell 0 --pf-er 0,1 --mix 0,1 > gpurun_out/sweep_r1d_$C.txt 2>gpurun_out/sweep_r1d_$C.err
-echo "$C rc=$?"
+#!/bin/bash
+# knob sweep + per-CTA phase profile: bash scripts/gpu_sweep.sh <tag> "<sweep args>" cfgs...
+TAG=$1; ARGS="$2"; shift 2
+OUT=gpurun_out; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1
+for C in "$@"; do
+  timeout 900 python scripts/kernel_sweep.py --config $C $ARGS > $OUT/sweep_${TAG}_$C.txt 2>$OUT/sweep_${TAG}_$C.err
+  echo "$C rc=$?"
 done

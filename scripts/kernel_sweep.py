@@ -39,22 +39,29 @@ def time_variant(dm, xr, y, reps, stream, fma=False):
     return ev0.elapsed_time(ev1) / reps * 1e3  # us
 
 
+STAMPS = ("start", "window", "ell_issued", "end", "own_er", "combine", "pool", "ell_published")
+
+
 def cta_profile(dm, xr, y, stream, n_ctas):
-    t = torch.zeros(n_ctas * 4, dtype=torch.int64, device=xr.device)
+    """Per-CTA phase stamps (us from the first CTA start): min / median / max."""
+    t = torch.zeros(n_ctas * 8, dtype=torch.int64, device=xr.device)
     dm.tune(timing=t)
     dm.spmv(xr, y, stream=stream)
     stream.synchronize()
     dm.tune(timing=None)
-    a = t.cpu().numpy().reshape(n_ctas, 4).astype(np.float64)
+    a = t.cpu().numpy().reshape(n_ctas, 8).astype(np.float64)
     t0 = a[:, 0].min()
-    rel = (a - t0) / 1e3  # us
     out = {}
-    for i, name in enumerate(("start", "window", "ell_drained", "end")):
-        col = rel[:, i]
-        out[name] = [round(float(np.min(col)), 2), round(float(np.median(col)), 2),
-                     round(float(np.max(col)), 2)]
+    for i, name in enumerate(STAMPS):
+        col = a[:, i]
+        col = col[col > 0]
+        if col.size == 0:
+            continue
+        rel = (col - t0) / 1e3
+        out[name] = [round(float(np.min(rel)), 2), round(float(np.median(rel)), 2),
+                     round(float(np.max(rel)), 2)]
     out["cta_duration_us"] = [round(float(v), 2) for v in
-                              np.percentile(rel[:, 3] - rel[:, 0], [0, 50, 90, 100])]
+                              np.percentile((a[:, 3] - a[:, 0]) / 1e3, [0, 50, 90, 100])]
     return out
 
 
@@ -68,7 +75,6 @@ def main():
     ap.add_argument("--er-warps", default="0,4")
     ap.add_argument("--ahead", default="0,3")
     ap.add_argument("--pf-ell", default="0,1")
-    ap.add_argument("--mix", default="0,1")
     ap.add_argument("--pf-er", default="0,1")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
@@ -93,24 +99,20 @@ def main():
     ewl = [int(v) for v in args.er_warps.split(",")]
     ahl = [int(v) for v in args.ahead.split(",")]
     pfl = [int(v) for v in args.pf_ell.split(",")]
-    mxl = [int(v) for v in args.mix.split(",")]
     pfrl = [int(v) for v in args.pf_er.split(",")]
     for (pool, ercost), h in handles.items():
-        for pfer, ew, ah, pfe, mx in itertools.product(pfrl, ewl, ahl, pfl, mxl):
-            if mx and ew != ewl[0]:
-                continue  # er_warps is unused in mix mode
-            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah,
-                   er_mix=mx)
+        for pfer, ew, ah, pfe in itertools.product(pfrl, ewl, ahl, pfl):
+            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
             results.append(dict(pool=pool, er_cost=ercost, pf_ell=pfe, pf_er=pfer, er_warps=ew,
-                                ahead=ah, mix=mx, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
+                                ahead=ah, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
                                 bitwise=ok))
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
     dm = handles[(best["pool"], best["er_cost"])]
     dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024,
-            er_warps=best["er_warps"], claim_ahead=best["ahead"], er_mix=best["mix"])
+            er_warps=best["er_warps"], claim_ahead=best["ahead"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
     us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
     print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,

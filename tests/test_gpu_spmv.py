@@ -207,3 +207,72 @@ def test_host_many_pipeline_matches_single_calls(user_order):
     assert dm.spmv_host_many([], user_order=user_order) == []
     with pytest.raises(ValueError, match="length mismatch"):
         dm.spmv_host_many([np.zeros(3)], user_order=user_order)
+
+
+def _fresh_handle(e, monkeypatch, long_row):
+    from paper_2204_06666_b200.device import DeviceMatrix
+
+    monkeypatch.setenv("EHYB_LONG_ROW", str(long_row))
+    return DeviceMatrix(e, 0)
+
+
+@pytest.mark.parametrize("tau", [4, 8])
+@pytest.mark.parametrize("case", ["hubs", "many", "warp4"])
+def test_long_rows_bitwise_strict_and_fma_tolerance(monkeypatch, tau, case):
+    # rows wider than EHYB_LONG_ROW leave the slice paths and run as whole-warp
+    # serial chains (strict) or reassociated segments (FMA mode)
+    if case == "hubs":
+        n, r, c, v = W.heavy_tail(k=16, n_hubs=4, min_len=200, max_len=3000)
+        prof, long_row = E.DeviceProfile(16, 32, 8192), 48
+    elif case == "many":  # most 27-point rows become long rows
+        n, r, c, v = W.permute_symmetric(*W.stencil27(16, 16, 16), seed=2)
+        prof, long_row = E.DeviceProfile(8, 32, 8192), 12
+    else:  # generic slice height
+        n, r, c, v = W.heavy_tail(k=10, n_hubs=3, min_len=50, max_len=400)
+        prof, long_row = E.DeviceProfile(8, 4, 8192), 16
+    m = E.CooMatrix(n, n, r, c, v)
+    e = E.build_ehyb(m, tau=tau, profile=prof)
+    dm = _fresh_handle(e, monkeypatch, long_row)
+    assert dm.info()["long_rows"] > 0
+    dt = dm.torch_dtype
+    for seed in (0, 1):
+        x = W.deterministic_vector(n, seed)
+        xr = E.permute_vector(x, e.plan)
+        want = c_oracle.spmv_ehyb(e, xr)
+        xt = torch.from_numpy(xr).to("cuda:0", dt)
+        for _ in range(3):  # repeated launches: per-launch counters reset
+            y = dm.spmv(xt)
+            torch.cuda.synchronize()
+            assert y.cpu().numpy().tobytes() == want.tobytes()
+        yf = dm.spmv(xt, fma=True)
+        yf2 = dm.spmv(xt, fma=True)
+        torch.cuda.synchronize()
+        assert yf.cpu().numpy().tobytes() == yf2.cpu().numpy().tobytes()  # deterministic
+        assert rel_error(yf.cpu().numpy(), want) <= (1e-12 if tau == 8 else 1e-5)
+    # non-finite x: the reference's padding products propagate NaN/inf
+    xb = E.permute_vector(W.deterministic_vector(n, 3), e.plan)
+    xb[0] = np.nan
+    xb[e.params.vec_cache_size] = np.inf
+    want = c_oracle.spmv_ehyb(e, xb)
+    y = dm.spmv(torch.from_numpy(xb).to("cuda:0", dt)).cpu().numpy()
+    assert np.array_equal(np.isnan(y), np.isnan(want))
+    fin = ~np.isnan(want)
+    assert y[fin].tobytes() == want[fin].tobytes()
+    dm.close()
+
+
+def test_persistent_ctas_multiple_partitions_per_cta():
+    # more partitions than resident CTAs (148 x 1 per SM): every CTA loops
+    # over several partitions, re-staging its window each time
+    n, r, c, v = W.permute_symmetric(*W.stencil27(40, 40, 40), seed=4)
+    m = E.CooMatrix(n, n, r, c, v)
+    e = E.build_ehyb(m, tau=8, profile=E.DeviceProfile(600, 32, 4096))
+    assert e.n_parts >= 600
+    dm = E.device_matrix(e, 0)
+    assert dm.info()["ctas"] < e.n_parts
+    x = W.deterministic_vector(n, 6)
+    xr = E.permute_vector(x, e.plan)
+    want = c_oracle.spmv_ehyb(e, xr)
+    for _ in range(3):
+        y, _ = E.spmv_ehyb(e, xr)
+        assert y.tobytes() == want.tobytes()
