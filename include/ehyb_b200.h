@@ -161,6 +161,7 @@ typedef struct ehyb_dev_info {
   int32_t er_buf_slices;      /* own ER slices buffered in shared memory per CTA */
   int32_t smem_bytes;         /* dynamic shared memory of a fused launch */
   int64_t long_rows;          /* rows computed by the long-row path (width > EHYB_LONG_ROW) */
+  int64_t ring_bytes;         /* shared-memory ring the ELL stream is TMA-staged through (0 = off) */
 } ehyb_dev_info;
 
 /* Upload an assembled matrix once (device = CUDA ordinal) and derive the

@@ -117,9 +117,16 @@ struct ehyb_dev {
   int32_t* pool_own_idx = nullptr;
   void* pool_acc = nullptr;
   unsigned int* pool_ctr = nullptr;
-  unsigned int epoch = 0;
+  unsigned int* epoch_dev = nullptr;  // [2] launch epoch, CTAs finished (device-side: graph-safe)
   // own-ER shared-memory buffer
-  int er_buf_slices = 0, er_buf_offset = 0, er_warps = 4;
+  int er_buf_slices = 0, er_buf_offset = 0, er_warps = 8;
+  size_t ring_offset = 0, ring_bytes = 0;  // ELL staging ring (0 = register path)
+  int ring_stages = 0, stage_bytes = 0, stage_vbytes = 0;
+  int32_t* part_stage_ptr = nullptr;  // ring stage plan (see SpmvParams)
+  int32_t* st_pos = nullptr;
+  int32_t* st_slots = nullptr;
+  int32_t* st_chunks = nullptr;
+  uint2* ch_stage = nullptr;
   int ell_ahead = 1, er_ahead = 1;
   // long rows (derived): masked out of the slice paths, computed by warps
   uint32_t* long_bits = nullptr;
@@ -146,7 +153,8 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, bx[0], bx[1], by[0], by[1], long_bits, lr_span,
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev,
+                    part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage, bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
                     lr_part, lr_cnt, lr_ctr};
     for (void* p : ptrs)
@@ -196,7 +204,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_own_ptr = h->pool_own_ptr;
   P.pool_own_idx = h->pool_own_idx;
   P.pool_acc = static_cast<T*>(h->pool_acc);
-  P.epoch = h->epoch;
+  P.epoch_dev = h->epoch_dev;
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
   P.er_warps = h->er_warps;
@@ -217,11 +225,31 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.lr_part = static_cast<T*>(h->lr_part);
   P.lr_cnt = h->lr_cnt;
   P.lr_ctr = h->lr_ctr;
-  auto kern = (do_ell && h->window_in_smem) ? spmv_fused_kernel<T, STRICT, C32, true>
-                              : spmv_fused_kernel<T, STRICT, C32, false>;
-  // dynamic smem: [window | own-ER buffer]; the buffer is only used when one
-  // launch runs both phases
-  const size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
+  void (*kern)(const SpmvParams<T>) = (do_ell && h->window_in_smem)
+                                           ? spmv_fused_kernel<T, STRICT, C32, true, false>
+                                           : spmv_fused_kernel<T, STRICT, C32, false, false>;
+  // dynamic smem: [window | own-ER buffer | ELL ring]; the buffer is only
+  // used when one launch runs both phases, the ring by any ELL launch
+  size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
+  P.ring_offset = 0;
+  P.ring_stages = P.stage_bytes = P.stage_vbytes = 0;
+  P.part_stage_ptr = P.st_pos = P.st_slots = P.st_chunks = nullptr;
+  P.ch_stage = nullptr;
+  if constexpr (C32) {
+    if (do_ell && h->window_in_smem && h->window_tma && h->ring_bytes > 0 && h->threads >= 64) {
+      kern = spmv_fused_kernel<T, STRICT, true, true, true>;
+      P.ring_offset = int32_t(h->ring_offset);
+      P.ring_stages = h->ring_stages;
+      P.stage_bytes = h->stage_bytes;
+      P.stage_vbytes = h->stage_vbytes;
+      P.part_stage_ptr = h->part_stage_ptr;
+      P.st_pos = h->st_pos;
+      P.st_slots = h->st_slots;
+      P.st_chunks = h->st_chunks;
+      P.ch_stage = h->ch_stage;
+      smem = h->ring_offset + h->ring_bytes;
+    }
+  }
   if (!(do_ell && do_er)) {
     P.er_buf_slices = 0;
   }
@@ -259,7 +287,6 @@ cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, boo
 
 cudaError_t launch_spmv(ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
                         cudaStream_t st) {
-  h->epoch += 1;  // per-launch counters alternate by epoch parity
   return h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
                      : launch_mode<double>(h, x, y, mode, ell, er, st);
 }
@@ -275,15 +302,15 @@ cudaError_t occupancy(const ehyb_dev* h, int* per_sm) {
   const bool c32 = h->warp == 32;
   const void* k;
   if (h->tau == 4)
-    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, true, true>
-                                 : (const void*)spmv_fused_kernel<float, true, true, false>)
-            : (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, false, true>
-                                 : (const void*)spmv_fused_kernel<float, true, false, false>);
+    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, true, true, false>
+                                 : (const void*)spmv_fused_kernel<float, true, true, false, false>)
+            : (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, false, true, false>
+                                 : (const void*)spmv_fused_kernel<float, true, false, false, false>);
   else
-    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, true, true>
-                                 : (const void*)spmv_fused_kernel<double, true, true, false>)
-            : (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, false, true>
-                                 : (const void*)spmv_fused_kernel<double, true, false, false>);
+    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, true, true, false>
+                                 : (const void*)spmv_fused_kernel<double, true, true, false, false>)
+            : (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, false, true, false>
+                                 : (const void*)spmv_fused_kernel<double, true, false, false, false>);
   if (h->smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
     if (e != cudaSuccess) return e;
@@ -354,9 +381,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   }
   std::sort(long_rows.begin(), long_rows.end());
   std::vector<uint32_t> lbits(size_t((h->local_rows + 31) / 32) + 1, 0u);
+  int64_t max_chunk_bytes = 0;  // widest ELL slice (after long rows), ring sizing
   for (int64_t r : long_rows) lbits[size_t((r - row_lo) >> 5)] |= 1u << ((r - row_lo) & 31);
+  std::vector<int32_t> eff(static_cast<size_t>(s_hi - s_lo));
   {
-    std::vector<int32_t> eff(size_t(s_hi - s_lo));
     for (int64_t s = s_lo; s < s_hi; ++s) {
       const int32_t W = m->width_ell[s];
       int32_t wmax = 0;
@@ -370,6 +398,8 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       if (e > kEffWidth) return fail("ELL slice width exceeds the device limit");
       if (has_long) e |= kEffHasLong | (wmax < W ? kEffPadTail : 0);
       eff[size_t(s - s_lo)] = e;
+      max_chunk_bytes = std::max<int64_t>(
+          max_chunk_bytes, (int64_t(e & kEffWidth) * int64_t(C) * int64_t(tb + 2) + 127) / 128 * 128);
     }
     CUDA_TRY(upload(&h->width_ell, eff.data(), eff.size() * 4, &h->bytes));
   }
@@ -402,7 +432,8 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       kMaxErBuf, (size_t(optin) - h->win_bytes - kStaticReserve) / (32 * tb)));
   h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
   const int64_t chunks = (vec + 31) / 32;
-  h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(32, chunks * 32)));
+  // one warp per chunk up to 1024 threads, plus the ring producer warp
+  h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(64, chunks * 32 + 32)));
   int per_sm = 0;
   CUDA_TRY(occupancy(h.get(), &per_sm));
   h->max_ctas = std::max<int64_t>(1, int64_t(per_sm) * h->sm_count);
@@ -466,6 +497,91 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     for (int64_t q = 0; q < n_loc_parts; ++q) max_own = std::max<int64_t>(max_own, int64_t(own[size_t(q)].size()));
     h->er_buf_slices = int(std::min<int64_t>(h->er_buf_slices, max_own));
     h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
+    // ELL ring (C == 32, TMA-staged window): shared memory left after the
+    // window, at least 2 chunks of the widest slice; the own-ER buffer gives
+    // way so the ring keeps >= EHYB_RING_KB (default 64 KB)
+    h->ring_bytes = 0;
+    if (C == 32 && h->window_tma && env_double("EHYB_RING", 0.0) != 0.0) {
+      cudaFuncAttributes fa{};
+      if (tb == 4)
+        CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<float, true, true, true, true>));
+      else
+        CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<double, true, true, true, true>));
+      const int64_t dyn = int64_t(optin) - int64_t(fa.sharedSizeBytes) - 256;
+      const int64_t avail = dyn - int64_t(h->win_bytes);
+      const int64_t want = std::max<int64_t>(2 * max_chunk_bytes,
+                                             int64_t(env_double("EHYB_RING_KB", 64.0) * 1024.0));
+      if (avail >= 2 * max_chunk_bytes && avail >= 16 * 1024) {
+        int64_t buf = int64_t(h->er_buf_slices) * 32 * int64_t(tb);
+        if (avail - buf < want) buf = std::max<int64_t>(0, avail - want);
+        h->er_buf_slices = int(buf / (32 * int64_t(tb)));
+        buf = int64_t(h->er_buf_slices) * 32 * int64_t(tb);
+        h->ring_offset = (size_t(h->win_bytes) + size_t(buf) + 127) / 128 * 128;
+        const int64_t total = (dyn - int64_t(h->ring_offset)) / 128 * 128;
+        // stages of ~EHYB_STAGE_KB (default 16 KB), 2..kRingNS-1 of them; each
+        // region must hold the widest chunk
+        const int64_t target = int64_t(env_double("EHYB_STAGE_KB", 16.0) * 1024.0);
+        int64_t ns = std::min<int64_t>(kRingNS - 1, std::max<int64_t>(2, total / std::max<int64_t>(target, 1)));
+        int64_t sb = total / ns / 128 * 128;
+        int64_t svb = sb * int64_t(tb) / int64_t(tb + 2) / 128 * 128;
+        const int64_t wmax = max_chunk_bytes / (32 * int64_t(tb + 2)) + 1;
+        if (ns >= 2 && svb >= 32 * wmax * int64_t(tb) && sb - svb >= 64 * wmax) {
+          h->ring_stages = int(ns);
+          h->stage_bytes = int(sb);
+          h->stage_vbytes = int(svb);
+          h->ring_bytes = size_t(ns * sb);
+        }
+        h->smem = h->win_bytes + size_t(buf);
+      }
+    }
+    if (h->ring_stages > 0) {
+      // stage plan: runs of consecutive chunks whose slab slots fit a stage's
+      // value and column regions; a slice narrowed by a long row ends its stage
+      // (its long lane's slots beyond the narrowed width are not copied)
+      const int64_t cpp = vec / 32;  // chunks per partition
+      const int64_t svb = h->stage_vbytes, scb = int64_t(h->stage_bytes) - h->stage_vbytes;
+      std::vector<int32_t> sptr(static_cast<size_t>(n_loc_parts) + 1, 0), spos, sslots, schunks;
+      std::vector<uint2> chs(static_cast<size_t>(n_loc_parts * cpp));
+      for (int64_t q = 0; q < n_loc_parts; ++q) {
+        sptr[size_t(q)] = int32_t(spos.size());
+        bool open = false;
+        int32_t cur_pos = 0, cur_slots = 0, cur_n = 0;
+        auto close = [&]() {
+          if (!open) return;
+          spos.push_back(cur_pos);
+          sslots.push_back(cur_slots);
+          schunks.push_back(cur_n);
+          open = false;
+        };
+        for (int64_t c = 0; c < cpp; ++c) {
+          const int64_t sl = q * cpp + c;
+          const int32_t e = eff[size_t(sl)];
+          const int64_t w = e & kEffWidth;
+          const int32_t p = pos[size_t(sl)];
+          int64_t rel = open ? int64_t(p) - cur_pos : 0;
+          if (open && ((rel + 32 * w) * int64_t(tb) > svb || (rel + 32 * w) * 2 > scb || cur_n >= 64)) {
+            close();
+            rel = 0;
+          }
+          if (!open) {
+            open = true;
+            cur_pos = p;
+            cur_n = 0;
+          }
+          chs[size_t(sl)] = make_uint2(uint32_t(int64_t(spos.size()) - sptr[size_t(q)]), uint32_t(rel));
+          cur_slots = int32_t(rel + 32 * w);
+          ++cur_n;
+          if (e & kEffHasLong) close();
+        }
+        close();
+      }
+      sptr[size_t(n_loc_parts)] = int32_t(spos.size());
+      CUDA_TRY(upload(&h->part_stage_ptr, sptr.data(), sptr.size() * 4, &h->bytes));
+      CUDA_TRY(upload(&h->st_pos, spos.data(), spos.size() * 4, &h->bytes));
+      CUDA_TRY(upload(&h->st_slots, sslots.data(), sslots.size() * 4, &h->bytes));
+      CUDA_TRY(upload(&h->st_chunks, schunks.data(), schunks.size() * 4, &h->bytes));
+      CUDA_TRY(upload(&h->ch_stage, chs.data(), chs.size() * 8, &h->bytes));
+    }
   }
   const int64_t n_sl = int64_t(order.size());
   std::vector<int64_t> epos(size_t(n_sl) + 1, 0);
@@ -621,6 +737,11 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(upload(&h->inverse, inv.data(), inv.size() * 4, &h->bytes));
   }
 
+  // ---- launch epoch on the device (starts at 1; the kernel advances it)
+  {
+    const unsigned int init[2] = {1u, 0u};
+    CUDA_TRY(upload(&h->epoch_dev, init, sizeof(init), &h->bytes));
+  }
   // ---- ER pool state: claim counters, per-owner lists, scratch, counts
   if (h->pool_hi > h->pool_lo) {
     std::vector<int32_t> optr(static_cast<size_t>(n_loc_parts) + 1, 0), oidx;
@@ -709,7 +830,8 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out) {
   out->sm_count = h->sm_count;
   out->pool_slices = h->pool_hi - h->pool_lo;
   out->er_buf_slices = h->er_buf_slices;
-  out->smem_bytes = int32_t(h->smem);
+  out->smem_bytes = int32_t(h->ring_bytes ? h->ring_offset + h->ring_bytes : h->smem);
+  out->ring_bytes = int64_t(h->ring_bytes);
   out->long_rows = h->lr_tasks;
   return 0;
 }

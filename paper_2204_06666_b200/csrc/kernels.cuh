@@ -66,12 +66,23 @@ struct SpmvParams {
   const int32_t* __restrict__ pool_own_ptr;  // [n_parts+1] pooled slices of each partition
   const int32_t* __restrict__ pool_own_idx;  // their slice indices
   T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
-  unsigned int epoch;               // launch sequence number (>= 1)
+  unsigned int* epoch_dev;          // [2]: launch sequence number (>= 1), CTAs finished; kept
+                                    // on the device so a captured CUDA graph replays correctly
   // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
   int32_t er_buf_slices;            // buffered own ER slices (<= kMaxErBuf)
   int32_t er_buf_offset;            // byte offset of the buffer in dynamic smem
   int32_t er_warps;                 // warps that start on ER before ELL
   int32_t n_parts;                  // partitions of this launch (grid may be smaller: CTAs loop)
+  int32_t ring_offset;              // RING variant: ELL staging ring in dynamic smem,
+  int32_t ring_stages, stage_bytes, stage_vbytes;  // stages x stage_bytes (values first)
+  // stage plan (host-built): stage t copies slab slots [st_pos[t], +st_slots[t])
+  // and holds st_chunks[t] consecutive chunks; chunk c of a partition lives in
+  // its local stage ch_stage[c].x at slot offset ch_stage[c].y
+  const int32_t* __restrict__ part_stage_ptr;  // [n_parts+1]
+  const int32_t* __restrict__ st_pos;
+  const int32_t* __restrict__ st_slots;
+  const int32_t* __restrict__ st_chunks;
+  const uint2* __restrict__ ch_stage;          // [local_rows/32]
   int32_t ell_ahead;                // 1 = claim the next ELL chunk (and its metadata) one ahead
   int32_t er_ahead;                 // 1 = same for ER slices
   // long rows (derived at upload): rows whose ELL or ER width exceeds the long
@@ -121,6 +132,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                              uint64_t* bar) {
@@ -243,6 +257,37 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
   }
   return acc;
 }
+
+// One 32-row SELL slice staged in shared memory by the ring producer (TMA):
+// values and columns are read with conflict-free LDS, x gathered from the
+// window; k ascending as in the reference.
+template <typename T, bool STRICT>
+__device__ __forceinline__ T ell_slice32_smem(const T* sv, const uint16_t* sc, int w,
+                                              const T* win) {
+  constexpr int U = 8;
+  T acc = T(0);
+  int k = 0;
+  for (; k + U <= w; k += U) {
+    uint32_t c[U];
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = sc[32 * (k + u)];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = sv[32 * (k + u)];
+    T xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = win[c[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = madd<STRICT>(acc, v[u], xv[u]);
+  }
+  for (; k < w; ++k) acc = madd<STRICT>(acc, sv[32 * k], win[sc[32 * k]]);
+  return acc;
+}
+
+constexpr int kRingNS = 8;   // max ring data slots
+constexpr int kRingFB = 64;  // full barriers, by stage number mod 64: a consumer (at most 31
+                             // chunks ahead of the oldest unconsumed one) never waits on a
+                             // barrier whose previous phase is still pending
 
 // Generic slice height C (the reference tests use 1, 4, 8): one row per
 // thread, slots pos + C k.
@@ -444,8 +489,8 @@ __device__ __forceinline__ T long_finish(const SpmvParams<T>& P, int task, T ell
 // STRICT mode (serial chains, longest first), segments in FMA mode (the last
 // segment of a row to finish sums the partials in segment order).
 template <typename T, bool STRICT>
-__device__ void long_rows_warp(const SpmvParams<T>& P, int lane, T* stage) {
-  unsigned int* ctr = P.lr_ctr + (P.epoch & 1u);
+__device__ void long_rows_warp(const SpmvParams<T>& P, int lane, T* stage, uint32_t ep) {
+  unsigned int* ctr = P.lr_ctr + (ep & 1u);
   const int n_items = STRICT ? P.lr_tasks : P.lr_segs;
   for (;;) {
     unsigned int v = 0;
@@ -486,10 +531,10 @@ __device__ void long_rows_warp(const SpmvParams<T>& P, int lane, T* stage) {
 // (release: the sums are visible before the count). At most `max_items`
 // slices (<= 0: until the pool is exhausted); returns false once exhausted.
 template <typename T, bool STRICT>
-__device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items) {
+__device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint32_t ep) {
   if (P.pool_hi <= P.pool_lo) return false;
-  unsigned int* ctr = P.pool_ctr + (P.epoch & 1u);
-  unsigned int* done = P.pool_done + (P.epoch & 1u) * uint32_t(P.n_parts);
+  unsigned int* ctr = P.pool_ctr + (ep & 1u);
+  unsigned int* done = P.pool_done + (ep & 1u) * uint32_t(P.n_parts);
   auto pclaim = [&]() -> int64_t {
     unsigned int v = 0;
     if (lane == 0) v = atomicAdd(ctr, 1u);
@@ -537,10 +582,17 @@ constexpr int kMaxErBuf = 2048;                        // buffered own ER slices
 // warp moves straight on to the partition's ER slices (no CTA barrier). An
 // ER row whose ELL chunk is still in flight waits on that chunk's done bit,
 // so y[r] = y_ell[r] + er_acc keeps the reference's order of operations.
-template <typename T, bool STRICT, bool C32, bool SMEM>
+template <typename T, bool STRICT, bool C32, bool SMEM, bool RING>
 __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T> P) {
+  static_assert(!RING || (C32 && SMEM), "the ELL ring needs 32-row slices and a staged window");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar;
+  // RING: ELL stages (runs of consecutive chunks, one bulk copy each for
+  // values and columns) streamed into shared memory by one producer warp
+  // (full: bytes landed; empty: every chunk of the stage consumed)
+  __shared__ uint64_t rfull[RING ? kRingFB : 1], rempty[RING ? kRingNS : 1];
+  __shared__ int rcount[RING ? kRingNS : 1];   // consumed chunks of the stage in the slot
+  __shared__ int rsize[RING ? kRingNS : 1];    // chunks of the stage in the slot
   __shared__ int next_chunk;
   __shared__ int next_er;
   __shared__ int next_comb;
@@ -549,24 +601,37 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   __shared__ uint32_t chunk_done[kMaxChunks / 32];
   __shared__ uint32_t er_done[kMaxErBuf / 32];
   __shared__ T lr_stage[64];  // long-row products (warp 0)
-
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int cta = blockIdx.x;
   const int64_t n_chunks = (P.vec + 31) >> 5;
   T* xs = reinterpret_cast<T*>(smem_raw);
 
+  __shared__ uint32_t s_ep;
   if (threadIdx.x == 0) {
+    // launch epoch (parity selects this launch's counters; the other parity
+    // is reset here for the next launch, which is stream-ordered after this)
+    const uint32_t e0 = *reinterpret_cast<volatile unsigned int*>(P.epoch_dev);
+    s_ep = e0;
     if (P.timing) P.timing[8 * cta] = globaltimer();
-    if (cta == 0 && P.pool_ctr) P.pool_ctr[(P.epoch + 1u) & 1u] = 0u;  // next launch's counter
-    if (cta == 0 && P.lr_ctr) P.lr_ctr[(P.epoch + 1u) & 1u] = 0u;
+    if (cta == 0 && P.pool_ctr) P.pool_ctr[(e0 + 1u) & 1u] = 0u;
+    if (cta == 0 && P.lr_ctr) P.lr_ctr[(e0 + 1u) & 1u] = 0u;
     if constexpr (SMEM) {
       if (P.window_tma) {
         mbar_init(&bar, 1);
+        if constexpr (RING) {
+          for (int i = 0; i < kRingFB; ++i) mbar_init(&rfull[i], 1);
+          for (int i = 0; i < kRingNS; ++i) mbar_init(&rempty[i], 1);
+        }
         fence_mbar_init();
       }
     }
   }
+  __syncthreads();
+  const uint32_t ep = s_ep;
+  // ring producer state (lane 0 of the last warp), kept across partitions
+  const int prod_warp = int(blockDim.x >> 5) - 1;
+  int64_t r_sbase = 0;  // stages of this CTA's earlier partitions (ring stage numbering)
 
   // Persistent over partitions: CTA b runs partitions b, b + grid, ... (one
   // pass when the grid covers every partition). A CTA waiting for pooled
@@ -587,7 +652,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
     next_pcomb = 0;
     ell_finished = 0;
     if (P.pool_done)  // the next launch's counter of this partition
-      P.pool_done[((P.epoch + 1u) & 1u) * uint32_t(P.n_parts) + uint32_t(part)] = 0u;
+      P.pool_done[((ep + 1u) & 1u) * uint32_t(P.n_parts) + uint32_t(part)] = 0u;
   }
   for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
     chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
@@ -635,7 +700,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   if (P.timing && threadIdx.x == 0 && !win_pending) P.timing[8 * cta + 1] = globaltimer();
   // long rows first (warp 0 of every CTA): their serial chains are the
   // longest dependent work of the launch
-  if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) long_rows_warp<T, STRICT>(P, lane, lr_stage);
+  if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) long_rows_warp<T, STRICT>(P, lane, lr_stage, ep);
 
   // own ER slices [s0, s1): the first n_buf are computed into a shared-memory
   // buffer at any time (ER-first warps overlap them with the ELL stream) and
@@ -755,7 +820,7 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
   };
 
   int64_t pending = -1;
-  if (P.do_er && P.do_ell && wid < P.er_warps) {  // ER-first warps
+  if (P.do_er && P.do_ell && wid < P.er_warps && !(RING && wid == prod_warp)) {  // ER-first warps
     if (n_buf > 0) {
       for (;;) {
         const int64_t idx = claim(&next_er);
@@ -767,9 +832,103 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
       }
     }
     // pooled slices of every partition, hidden behind the other warps' ELL stream
-    pool_drain<T, STRICT>(P, lane, 0);
+    pool_drain<T, STRICT>(P, lane, 0, ep);
   }
-  if (P.do_ell) {
+  const int64_t st_lo = RING ? int64_t(__ldg(P.part_stage_ptr + part)) : 0;
+  const int64_t n_st = RING ? int64_t(__ldg(P.part_stage_ptr + part + 1)) - st_lo : 0;
+  if (RING && P.do_ell && wid == prod_warp) {
+    // producer: stage sg = r_sbase + t into data slot sg % ring_stages once
+    // the slot's previous stage is consumed; one bulk copy per region
+    unsigned char* rbase = smem_raw + P.ring_offset;
+    const int64_t ns = P.ring_stages;
+    int32_t m_pos = 0, m_slots = 0, m_nch = 0;
+    for (int64_t t = 0; t < n_st; ++t) {
+      if ((t & 31) == 0) {  // the next 32 stages' plan, one load per lane
+        const bool ok = t + lane < n_st;
+        m_pos = ok ? __ldg(P.st_pos + st_lo + t + lane) : 0;
+        m_slots = ok ? __ldg(P.st_slots + st_lo + t + lane) : 0;
+        m_nch = ok ? __ldg(P.st_chunks + st_lo + t + lane) : 0;
+      }
+      const int32_t pos = __shfl_sync(0xffffffffu, m_pos, int(t & 31));
+      const int32_t slots = __shfl_sync(0xffffffffu, m_slots, int(t & 31));
+      const int32_t nch = __shfl_sync(0xffffffffu, m_nch, int(t & 31));
+      if (lane == 0) {
+        const int64_t sg = r_sbase + t;
+        const int sl = int(sg % ns);
+        if (sg >= ns) {
+          const unsigned long long tw = P.timing ? globaltimer() : 0ull;
+          mbar_wait(&rempty[sl], uint32_t(sg / ns - 1) & 1u);
+          if (P.timing) {  // dev profile: producer time blocked on a full ring, waits
+            atomicAdd(P.timing + 8 * cta + 5, globaltimer() - tw);
+            atomicAdd(P.timing + 8 * cta + 6, 1ull);
+          }
+        }
+        unsigned char* dst = rbase + int64_t(sl) * P.stage_bytes;
+        rcount[sl] = 0;
+        rsize[sl] = nch;
+        uint64_t* fb = &rfull[sg % kRingFB];
+        if (slots > 0) {
+          const uint32_t vb = uint32_t(slots) * uint32_t(sizeof(T)), cb = uint32_t(slots) * 2u;
+          mbar_expect_tx(fb, vb + cb);
+          tma_bulk_g2s(dst, P.val_ell + pos, vb, fb);
+          tma_bulk_g2s(dst + P.stage_vbytes, P.col_ell + pos, cb, fb);
+        } else {
+          mbar_arrive(fb);
+        }
+      }
+    }
+    if (P.timing && lane == 0) P.timing[8 * cta + 2] = globaltimer();
+    __syncwarp();
+  } else if (RING && P.do_ell) {
+    // consumers: chunks in claim order, read from their stage in the ring
+    // (chunk metadata one claim ahead)
+    const unsigned char* rbase = smem_raw + P.ring_offset;
+    const int64_t ns = P.ring_stages;
+    auto rmeta = [&](int64_t c, int32_t& eff, uint2& cs) {
+      if (c < n_chunks) {
+        eff = __ldg(P.width_ell + (row0 >> 5) + c);
+        cs = __ldg(P.ch_stage + (row0 >> 5) + c);
+      }
+    };
+    int64_t chunk = claim(&next_chunk);
+    int32_t eff = 0;
+    uint2 cs = make_uint2(0u, 0u);
+    rmeta(chunk, eff, cs);
+    while (chunk < n_chunks) {
+      const int64_t nxt = claim(&next_chunk);
+      int32_t eff_n = 0;
+      uint2 cs_n = make_uint2(0u, 0u);
+      rmeta(nxt, eff_n, cs_n);
+      const int64_t sg = r_sbase + int64_t(cs.x);
+      mbar_wait(&rfull[sg % kRingFB], uint32_t(sg / kRingFB) & 1u);
+      const int sl = int(sg % ns);
+      const int w = eff & kEffWidth;
+      const unsigned char* base = rbase + int64_t(sl) * P.stage_bytes;
+      const T* sv = reinterpret_cast<const T*>(base) + cs.y;
+      const uint16_t* sc = reinterpret_cast<const uint16_t*>(base + P.stage_vbytes) + cs.y;
+      if (win_pending) {
+        mbar_wait(&bar, phase);
+        win_pending = false;
+        if (P.timing && threadIdx.x == 0) P.timing[8 * cta + 1] = globaltimer();
+      }
+      T acc = ell_slice32_smem<T, STRICT>(sv + lane, sc + lane, w, win);
+      __syncwarp();
+      if (lane == 0 && atomicAdd(&rcount[sl], 1) == rsize[sl] - 1)
+        mbar_arrive(&rempty[sl]);  // the whole stage is consumed
+      bool store = true;
+      if (eff & (kEffPadTail | kEffHasLong)) {
+        if (eff & kEffPadTail) acc = add_rn(acc, mul_rn(T(0), win[0]));
+        store = !((__ldg(P.long_bits + (row0 >> 5) + chunk) >> lane) & 1u);
+      }
+      publish();
+      if (store) P.y[row0 + chunk * 32 + lane] = acc;
+      unpublished = chunk;
+      chunk = nxt;
+      eff = eff_n;
+      cs = cs_n;
+    }
+    publish();
+  } else if (P.do_ell) {
     int64_t chunk = claim(&next_chunk);
     if (P.ell_ahead) {
       EllMeta m = ell_meta(chunk);
@@ -805,10 +964,11 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
         finish_own_er(idx, er_meta(s0 + idx, s1));
     }
     auto stamp = [&](int i) {
-      if (P.timing && lane == 0) atomicMax(P.timing + 8 * cta + i, globaltimer());
+      if (P.timing && lane == 0 && !(RING && (i == 5 || i == 6)))
+        atomicMax(P.timing + 8 * cta + i, globaltimer());
     };
     stamp(4);
-    pool_drain<T, STRICT>(P, lane, 0);  // whatever the ER-first warps left
+    pool_drain<T, STRICT>(P, lane, 0, ep);  // whatever the ER-first warps left
     // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
     for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
       while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
@@ -827,9 +987,9 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
     const int32_t q1 = P.pool_own_ptr ? __ldg(P.pool_own_ptr + part + 1) : 0;
     if (q1 > q0) {
       const unsigned int* done =
-          P.pool_done + (P.epoch & 1u) * uint32_t(P.n_parts) + uint32_t(part);
+          P.pool_done + (ep & 1u) * uint32_t(P.n_parts) + uint32_t(part);
       while (ld_acquire_gpu(done) != unsigned(q1 - q0)) {
-        if (!pool_drain<T, STRICT>(P, lane, 1)) __nanosleep(128);  // help, else wait
+        if (!pool_drain<T, STRICT>(P, lane, 1, ep)) __nanosleep(128);  // help, else wait
       }
       for (int64_t idx = claim(&next_pcomb); idx < q1 - q0; idx = claim(&next_pcomb)) {
         const int64_t sl = __ldg(P.pool_own_idx + q0 + idx);
@@ -843,11 +1003,18 @@ __global__ void __launch_bounds__(1024, 1) spmv_fused_kernel(const SpmvParams<T>
     }
     stamp(6);
   }
+  r_sbase += n_st;
   }  // partitions of this CTA
 
-  if (P.timing) {
-    __syncthreads();
-    if (threadIdx.x == 0) P.timing[8 * cta + 3] = globaltimer();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (P.timing) P.timing[8 * cta + 3] = globaltimer();
+    // the last CTA to finish advances the launch epoch
+    __threadfence();
+    if (atomicAdd(P.epoch_dev + 1, 1u) == gridDim.x - 1) {
+      P.epoch_dev[1] = 0u;
+      P.epoch_dev[0] = ep + 1u;
+    }
   }
 }
 

@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r1l.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_spmv.py -x -q -k "corpus or small_bitwise or long_rows" > gpurun_out/pytest_r1l.log 2>&1; echo "pytest rc=$?"
+bash scripts/gpu_sweep.sh r1l "--pool 0.95 --er-cost 5.0 --er-warps 8 --ahead 3 --pf-ell 0 --pf-er 1 --ring 1 --stage-kb 8,16,32" cfg3f32 cfg2

@@ -60,6 +60,7 @@ def cta_profile(dm, xr, y, stream, n_ctas):
         rel = (col - t0) / 1e3
         out[name] = [round(float(np.min(rel)), 2), round(float(np.median(rel)), 2),
                      round(float(np.max(rel)), 2)]
+    out["raw_col5_col6_median"] = [float(np.median(a[:, 5])), float(np.median(a[:, 6]))]
     out["cta_duration_us"] = [round(float(v), 2) for v in
                               np.percentile((a[:, 3] - a[:, 0]) / 1e3, [0, 50, 90, 100])]
     return out
@@ -76,6 +77,8 @@ def main():
     ap.add_argument("--ahead", default="0,3")
     ap.add_argument("--pf-ell", default="0,1")
     ap.add_argument("--pf-er", default="0,1")
+    ap.add_argument("--ring", default="0", help="EHYB_RING values (0 = register ELL path)")
+    ap.add_argument("--stage-kb", default="16", help="EHYB_STAGE_KB values")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
     gold = bench.golden_y_digest(args.config)
@@ -92,25 +95,31 @@ def main():
     from paper_2204_06666_b200.device import DeviceMatrix
 
     handles = {}
-    for pool, ercost in itertools.product(args.pool.split(","), args.er_cost.split(",")):
+    for pool, ercost, ring, skb in itertools.product(args.pool.split(","), args.er_cost.split(","),
+                                                     args.ring.split(","), args.stage_kb.split(",")):
+        if ring == "0" and skb != args.stage_kb.split(",")[0]:
+            continue
         os.environ["EHYB_POOL_FACTOR"] = pool
         os.environ["EHYB_ER_COST"] = ercost
-        handles[(pool, ercost)] = DeviceMatrix(e, 0)
+        os.environ["EHYB_RING"] = ring
+        os.environ["EHYB_STAGE_KB"] = skb
+        handles[(pool, ercost, ring, skb)] = DeviceMatrix(e, 0)
     ewl = [int(v) for v in args.er_warps.split(",")]
     ahl = [int(v) for v in args.ahead.split(",")]
     pfl = [int(v) for v in args.pf_ell.split(",")]
     pfrl = [int(v) for v in args.pf_er.split(",")]
-    for (pool, ercost), h in handles.items():
+    for (pool, ercost, ring, skb), h in handles.items():
         for pfer, ew, ah, pfe in itertools.product(pfrl, ewl, ahl, pfl):
             h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
-            results.append(dict(pool=pool, er_cost=ercost, pf_ell=pfe, pf_er=pfer, er_warps=ew,
+            results.append(dict(pool=pool, er_cost=ercost, ring=ring, stage_kb=skb,
+                                ring_kb=h.info()["ring_bytes"] // 1024, pf_ell=pfe, pf_er=pfer, er_warps=ew,
                                 ahead=ah, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
                                 bitwise=ok))
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
-    dm = handles[(best["pool"], best["er_cost"])]
+    dm = handles[(best["pool"], best["er_cost"], best["ring"], best["stage_kb"])]
     dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024,
             er_warps=best["er_warps"], claim_ahead=best["ahead"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
