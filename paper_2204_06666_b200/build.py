@@ -36,6 +36,8 @@ def _stale(target: str, deps) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
+    if os.environ.get("EHYB_NVCC_FLAGS"):
+        force = True
     if not force and not _stale(LIB, deps):
         return LIB
     cmd = [
@@ -43,6 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-Xcompiler", "-fPIC,-fopenmp,-O3,-fvisibility=hidden",
         "-Xptxas", "-v" if verbose else "-O3",
         "-I", os.path.join(ROOT, "include"),
+        *os.environ.get("EHYB_NVCC_FLAGS", "").split(),  # dev experiments (-D knobs)
         *[os.path.join(CSRC, f) for f in SOURCES],
         "-o", LIB + ".tmp",
         "-lcusparse", "-lgomp",

@@ -122,6 +122,7 @@ struct ehyb_dev {
   int er_buf_slices = 0, er_buf_offset = 0, er_warps = 8;
   size_t ring_offset = 0, ring_bytes = 0;  // ELL staging ring (0 = register path)
   int ring_stages = 0, stage_bytes = 0, stage_vbytes = 0;
+  bool ell_vec = false;  // ELL slices in the 128-bit interleaved layout
   int32_t* part_stage_ptr = nullptr;  // ring stage plan (see SpmvParams)
   int32_t* st_pos = nullptr;
   int32_t* st_slots = nullptr;
@@ -212,6 +213,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.ell_ahead = h->ell_ahead;
   P.er_ahead = h->er_ahead;
   P.long_bits = h->long_bits;
+  P.ell_vec = h->ell_vec ? 1 : 0;
   P.lr_tasks = h->lr_tasks;
   P.lr_span = h->lr_span;
   P.lr_row = h->lr_row;
@@ -359,9 +361,6 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::vector<int32_t> pos(size_t(s_hi - s_lo) + 1);
   for (int64_t s = s_lo; s <= s_hi; ++s) pos[size_t(s - s_lo)] = int32_t(m->position_ell[s] - base);
   CUDA_TRY(upload(&h->pos_ell, pos.data(), pos.size() * 4, &h->bytes));
-  CUDA_TRY(upload(&h->val_ell, static_cast<const char*>(m->val_ell) + size_t(base) * tb,
-                  size_t(slots) * tb, &h->bytes));
-  CUDA_TRY(upload(&h->col_ell, m->col_ell + base, size_t(slots) * 2, &h->bytes));
 
   // ---- long rows: ELL or ER width above the threshold. They leave the slice
   // paths (lane masked, slice narrowed to its widest remaining lane) and are
@@ -405,6 +404,41 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   }
   CUDA_TRY(upload(&h->long_bits, lbits.data(), lbits.size() * 4, &h->bytes));
 
+  // ---- ELL slab. C == 32: each slice is re-laid so a lane's 4 consecutive k
+  // are contiguous (one 128-bit value load per 4 (fp32) or 2 (fp64) entries,
+  // one 64-bit load per 4 columns; the W % 4 tail keeps the SELL layout).
+  // Same slots, same per-slice positions; slices narrowed by a long row keep
+  // the reference layout. A derived device layout, never a parity object.
+  h->ell_vec = C == 32 && env_double("EHYB_VEC", 0.0) != 0.0 && env_double("EHYB_RING", 0.0) == 0.0;
+  if (h->ell_vec) {
+    std::vector<char> pv(size_t(std::max<int64_t>(slots, 1)) * tb);
+    std::vector<uint16_t> pc(size_t(std::max<int64_t>(slots, 1)));
+    const char* sv = static_cast<const char*>(m->val_ell) + size_t(base) * tb;
+    const uint16_t* sc = m->col_ell + base;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t s = s_lo; s < s_hi; ++s) {
+      const int64_t p0 = pos[size_t(s - s_lo)];
+      const int64_t W = m->width_ell[s];
+      const bool keep = (eff[size_t(s - s_lo)] & kEffHasLong) != 0;
+      const int64_t nb = W / 4;
+      for (int64_t k = 0; k < W; ++k)
+        for (int64_t lane = 0; lane < 32; ++lane) {
+          const int64_t src = p0 + lane + 32 * k;
+          const int64_t dst = keep ? src
+                                   : p0 + (k < 4 * nb ? (k / 4) * 128 + lane * 4 + (k % 4)
+                                                      : 128 * nb + (k - 4 * nb) * 32 + lane);
+          std::memcpy(&pv[size_t(dst) * tb], sv + size_t(src) * tb, tb);
+          pc[size_t(dst)] = sc[src];
+        }
+    }
+    CUDA_TRY(upload(&h->val_ell, pv.data(), size_t(slots) * tb, &h->bytes));
+    CUDA_TRY(upload(&h->col_ell, pc.data(), size_t(slots) * 2, &h->bytes));
+  } else {
+    CUDA_TRY(upload(&h->val_ell, static_cast<const char*>(m->val_ell) + size_t(base) * tb,
+                    size_t(slots) * tb, &h->bytes));
+    CUDA_TRY(upload(&h->col_ell, m->col_ell + base, size_t(slots) * 2, &h->bytes));
+  }
+
   // ---- ER regrouped per owning partition
   const int64_t n_loc_parts = p1 - p0;
   std::vector<std::vector<int64_t>> members(static_cast<size_t>(n_loc_parts));
@@ -433,7 +467,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
   const int64_t chunks = (vec + 31) / 32;
   // one warp per chunk up to 1024 threads, plus the ring producer warp
-  h->threads = int(std::min<int64_t>(1024, std::max<int64_t>(64, chunks * 32 + 32)));
+  h->threads = int(std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, chunks * 32 + 32)));
   int per_sm = 0;
   CUDA_TRY(occupancy(h.get(), &per_sm));
   h->max_ctas = std::max<int64_t>(1, int64_t(per_sm) * h->sm_count);
@@ -802,7 +836,8 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
     case EHYB_TUNE_PREFETCH_ELL: h->pf_ell = int(std::max<int64_t>(0, value)); return 0;
     case EHYB_TUNE_PREFETCH_ER: h->pf_er = value ? 1 : 0; return 0;
     case EHYB_TUNE_THREADS:
-      if (value < 32 || value > 1024 || value % 32) return fail("threads must be a multiple of 32 in [32, 1024]");
+      if (value < 32 || value > kMaxThreads || value % 32)
+        return fail("threads must be a multiple of 32 in [32, " + std::to_string(kMaxThreads) + "]");
       h->threads = int(value);
       return 0;
     case EHYB_TUNE_ER_WARPS: h->er_warps = int(std::max<int64_t>(0, value)); return 0;

@@ -241,3 +241,143 @@ def read_ehyb_container(source):
     except ValueError as exc:
         raise ContainerError(f"inconsistent container contents: {exc}") from exc
     return e
+
+
+# --------------------------------------------------------------------------
+# Matrix Market text (reference matrix_io.py:111-252), parsed with numpy
+# --------------------------------------------------------------------------
+
+def _mm_text(source) -> str:
+    import os
+
+    if isinstance(source, (str, os.PathLike)):
+        with open(source, "rb") as fh:
+            return fh.read().decode("latin-1")
+    if isinstance(source, (bytes, bytearray)):
+        return bytes(source).decode("latin-1")
+    data = source.read()
+    return data.decode("latin-1") if isinstance(data, bytes) else data
+
+
+def parse_matrix_market(source) -> CooMatrix:
+    """Matrix Market "coordinate" text -> CooMatrix (reference contract,
+    matrix_io.py:123-231): path, bytes or file object; symmetric input
+    mirrored to general storage, pattern entries valued 1.0, 1-based indices
+    made 0-based, duplicates summed (entries end up sorted by (row, col)).
+    Errors name the offending line: MatrixMarketError for malformed input,
+    UnsupportedFormatError for complex / array / other symmetries.
+
+    Entry lines are converted in one vectorised pass; only malformed input
+    falls back to a line-by-line scan to name the line."""
+    lines = _mm_text(source).splitlines()
+    if not lines:
+        raise MatrixMarketError("line 1: empty input")
+    head = lines[0].strip().split()
+    if len(head) != 5 or head[0].lower() != "%%matrixmarket":
+        raise MatrixMarketError("line 1: malformed Matrix Market header")
+    obj, fmt, field, symmetry = (t.lower() for t in head[1:])
+    if obj != "matrix":
+        raise MatrixMarketError(f"line 1: unsupported object {obj!r}")
+    if fmt == "array":
+        raise UnsupportedFormatError("line 1: dense 'array' files are not supported")
+    if fmt != "coordinate":
+        raise MatrixMarketError(f"line 1: unknown format {fmt!r}")
+    if field == "complex":
+        raise UnsupportedFormatError("line 1: complex-valued matrices are not supported")
+    if field not in ("real", "integer", "pattern"):
+        raise MatrixMarketError(f"line 1: unknown field {field!r}")
+    if symmetry not in ("general", "symmetric"):
+        raise UnsupportedFormatError(f"line 1: unsupported symmetry {symmetry!r}")
+    i = 1
+    while True:
+        if i >= len(lines):
+            raise MatrixMarketError(f"line {i + 1}: missing size line")
+        text = lines[i].strip()
+        i += 1
+        if text and not text.startswith("%"):
+            break
+    tok = text.split()
+    if len(tok) != 3:
+        raise MatrixMarketError(f"line {i}: size line must be 'rows cols nnz'")
+    try:
+        n_rows, n_cols, n_decl = (int(t) for t in tok)
+    except ValueError:
+        raise MatrixMarketError(f"line {i}: size line must contain integers") from None
+    if min(n_rows, n_cols, n_decl) < 0:
+        raise MatrixMarketError(f"line {i}: negative size")
+    pattern = field == "pattern"
+    want = 2 if pattern else 3
+    body = [(k + 1, ln) for k, ln in enumerate(lines[i:], start=i)
+            if ln.strip() and not ln.lstrip().startswith("%")]
+    try:
+        if len(body) != n_decl:
+            raise ValueError
+        rows = np.empty(n_decl, np.int64)
+        cols = np.empty(n_decl, np.int64)
+        vals = np.ones(n_decl, np.float64)
+        if n_decl:
+            fields = [ln.split() for _, ln in body]
+            if min(len(f) for f in fields) < want:
+                raise ValueError
+            rows[:] = np.array([f[0] for f in fields], dtype=np.int64)
+            cols[:] = np.array([f[1] for f in fields], dtype=np.int64)
+            if not pattern:
+                vals[:] = np.array([f[2] for f in fields], dtype=np.float64)
+            if (rows.min() < 1 or rows.max() > n_rows or cols.min() < 1
+                    or cols.max() > n_cols):
+                raise ValueError
+    except (ValueError, OverflowError):
+        _mm_locate_error(body, n_rows, n_cols, n_decl, want, pattern, len(lines))
+        raise MatrixMarketError("malformed entries") from None
+    r, c, v = rows - 1, cols - 1, vals
+    if symmetry == "symmetric":
+        off = r != c
+        r, c, v = (np.concatenate([r, c[off]]), np.concatenate([c, r[off]]),
+                   np.concatenate([v, v[off]]))
+    if r.size:
+        key = r * np.int64(max(n_cols, 1)) + c
+        uniq, inverse = np.unique(key, return_inverse=True)
+        summed = np.zeros(uniq.size, np.float64)
+        np.add.at(summed, inverse, v)
+        r, c, v = uniq // max(n_cols, 1), uniq % max(n_cols, 1), summed
+    return CooMatrix(n_rows, n_cols, r, c, v)
+
+
+def _mm_locate_error(body, n_rows, n_cols, n_decl, want, pattern, n_lines):
+    """Line-by-line scan reproducing the reference's error messages."""
+    for seen, (lineno, ln) in enumerate(body):
+        if seen == n_decl:
+            raise MatrixMarketError(f"line {lineno}: extra entry beyond the declared {n_decl}")
+        t = ln.split()
+        if len(t) < want:
+            raise MatrixMarketError(f"line {lineno}: expected {want} fields per entry")
+        try:
+            a, b = int(t[0]), int(t[1])
+            if not pattern:
+                float(t[2])
+        except ValueError:
+            raise MatrixMarketError(f"line {lineno}: malformed entry") from None
+        if not (1 <= a <= n_rows and 1 <= b <= n_cols):
+            raise MatrixMarketError(f"line {lineno}: index out of declared bounds")
+    if len(body) != n_decl:
+        raise MatrixMarketError(f"line {n_lines}: expected {n_decl} entries, found {len(body)}")
+
+
+def write_matrix_market(m: CooMatrix, sink) -> None:
+    """CooMatrix -> Matrix Market coordinate/real/general text, entries in
+    (row, col) order, values with 17 significant digits (matrix_io.py:234-252)."""
+    import os
+
+    order = np.lexsort((m.cols, m.rows))
+    body = "\n".join(f"{a} {b} {x:.17g}" for a, b, x in
+                     zip(m.rows[order] + 1, m.cols[order] + 1, m.values[order]))
+    text = (f"%%MatrixMarket matrix coordinate real general\n{m.n_rows} {m.n_cols} {m.nnz}\n"
+            + (body + "\n" if m.nnz else ""))
+    if isinstance(sink, (str, os.PathLike)):
+        with open(sink, "w") as fh:
+            fh.write(text)
+    else:
+        try:
+            sink.write(text)
+        except TypeError:
+            sink.write(text.encode("ascii"))

@@ -79,6 +79,7 @@ def main():
     ap.add_argument("--pf-er", default="0,1")
     ap.add_argument("--ring", default="0", help="EHYB_RING values (0 = register ELL path)")
     ap.add_argument("--stage-kb", default="16", help="EHYB_STAGE_KB values")
+    ap.add_argument("--vec", default="0", help="EHYB_VEC values (0 = SELL layout, scalar loads)")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
     gold = bench.golden_y_digest(args.config)
@@ -95,34 +96,56 @@ def main():
     from paper_2204_06666_b200.device import DeviceMatrix
 
     handles = {}
-    for pool, ercost, ring, skb in itertools.product(args.pool.split(","), args.er_cost.split(","),
-                                                     args.ring.split(","), args.stage_kb.split(",")):
+    for pool, ercost, ring, skb, vec in itertools.product(
+            args.pool.split(","), args.er_cost.split(","), args.ring.split(","),
+            args.stage_kb.split(","), args.vec.split(",")):
         if ring == "0" and skb != args.stage_kb.split(",")[0]:
             continue
+        os.environ["EHYB_VEC"] = vec
         os.environ["EHYB_POOL_FACTOR"] = pool
         os.environ["EHYB_ER_COST"] = ercost
         os.environ["EHYB_RING"] = ring
         os.environ["EHYB_STAGE_KB"] = skb
-        handles[(pool, ercost, ring, skb)] = DeviceMatrix(e, 0)
+        handles[(pool, ercost, ring, skb, vec)] = DeviceMatrix(e, 0)
     ewl = [int(v) for v in args.er_warps.split(",")]
     ahl = [int(v) for v in args.ahead.split(",")]
     pfl = [int(v) for v in args.pf_ell.split(",")]
     pfrl = [int(v) for v in args.pf_er.split(",")]
-    for (pool, ercost, ring, skb), h in handles.items():
+    for (pool, ercost, ring, skb, vec), h in handles.items():
         for pfer, ew, ah, pfe in itertools.product(pfrl, ewl, ahl, pfl):
-            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=1024, er_warps=ew, claim_ahead=ah)
+            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=int(os.environ.get('EHYB_THREADS', '1024')), er_warps=ew, claim_ahead=ah)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
-            results.append(dict(pool=pool, er_cost=ercost, ring=ring, stage_kb=skb,
+            results.append(dict(pool=pool, er_cost=ercost, ring=ring, stage_kb=skb, vec=vec,
                                 ring_kb=h.info()["ring_bytes"] // 1024, pf_ell=pfe, pf_er=pfer, er_warps=ew,
                                 ahead=ah, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
                                 bitwise=ok))
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
-    dm = handles[(best["pool"], best["er_cost"], best["ring"], best["stage_kb"])]
-    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=1024,
+    dm = handles[(best["pool"], best["er_cost"], best["ring"], best["stage_kb"], best["vec"])]
+    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=int(os.environ.get('EHYB_THREADS', '1024')),
             er_warps=best["er_warps"], claim_ahead=best["ahead"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
+    # the two phases on their own (split launches): what each costs in isolation
+    import ctypes as C
+    from paper_2204_06666_b200 import _lib as L
+
+    def phase_us(name):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        st = C.c_void_p(stream.cuda_stream)
+        xp, yp = C.c_void_p(xr.data_ptr()), C.c_void_p(y.data_ptr())
+        for _ in range(10):
+            L.call(name, dm.handle, xp, yp, L.MODE_STRICT, st)
+        ev0.record(stream)
+        for _ in range(args.reps):
+            L.call(name, dm.handle, xp, yp, L.MODE_STRICT, st)
+        ev1.record(stream)
+        ev1.synchronize()
+        return round(ev0.elapsed_time(ev1) / args.reps * 1e3, 2)
+
+    prof["ell_only_us"] = phase_us("ehyb_dev_spmv_ell")
+    prof["er_only_us"] = phase_us("ehyb_dev_spmv_er")
     us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
     print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,
                       "fma_us": round(us_fma, 2), "bmin": bmin}), flush=True)
