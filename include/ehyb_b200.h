@@ -277,6 +277,14 @@ EHYB_API int ehyb_dev_cg_xr(void* x, void* r, const void* p, const void* q, cons
 EHYB_API int ehyb_dev_cg_p(void* p, const void* r, const double* rr_new, const double* rr_old,
                            int64_t n, int32_t tau, void* stream);
 /* y = a*x + y (a read from device memory, scaled by sign). */
+/* Chronopoulos-Gear CG (one all-reduce per iteration): two fp64 dot
+ * products in one pass, out2_dev = {a.b, c.d}; and one step's scalar update
+ * (sc = {gamma, delta, gamma_old, alpha, beta} on the device) fused with
+ * p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s. */
+EHYB_API int ehyb_dev_dot2(const void* a, const void* b, const void* c, const void* d, int64_t n,
+                           int32_t tau, double* out2_dev, void* stream);
+EHYB_API int ehyb_dev_cgcg_step(void* x, void* r, void* p, void* s, const void* w, double* sc,
+                                int first, int64_t n, int32_t tau, void* stream);
 EHYB_API int ehyb_dev_axpy(const double* a_dev, double sign, const void* x, void* y, int64_t n,
                            int32_t tau, void* stream);
 

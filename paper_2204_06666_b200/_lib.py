@@ -113,6 +113,8 @@ _PROTOS = {
     "ehyb_dev_dot": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp, vp]),
     "ehyb_dev_cg_xr": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp]),
     "ehyb_dev_cg_p": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int32, vp]),
+    "ehyb_dev_dot2": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp]),
+    "ehyb_dev_cgcg_step": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int64, C.c_int32, vp]),
     "ehyb_dev_axpy":(C.c_int, [vp, C.c_double, vp, vp, C.c_int64, C.c_int32, vp]),
     "ehyb_csr_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_int32,
                                   C.c_int, C.POINTER(vp)]),

@@ -1141,6 +1141,51 @@ EHYB_API int ehyb_dev_cg_p(void* p, const void* r, const double* rr_new, const d
   EHYB_CATCH
 }
 
+EHYB_API int ehyb_dev_dot2(const void* a, const void* b, const void* c, const void* d, int64_t n,
+                           int32_t tau, double* out2_dev, void* stream) {
+  EHYB_TRY {
+    auto st = static_cast<cudaStream_t>(stream);
+    constexpr int kBlocks = 592, kThreads = 512;
+    static thread_local std::unordered_map<int, double*> partials;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    double*& part = partials[dev];
+    if (!part) CUDA_TRY(cudaMalloc(&part, 2 * kBlocks * sizeof(double)));
+    if (tau == 4)
+      dot2_partial_kernel<float><<<kBlocks, kThreads, 0, st>>>(
+          static_cast<const float*>(a), static_cast<const float*>(b), static_cast<const float*>(c),
+          static_cast<const float*>(d), n, part);
+    else
+      dot2_partial_kernel<double><<<kBlocks, kThreads, 0, st>>>(
+          static_cast<const double*>(a), static_cast<const double*>(b),
+          static_cast<const double*>(c), static_cast<const double*>(d), n, part);
+    dot2_final_kernel<<<1, 1024, 0, st>>>(part, kBlocks, out2_dev);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_cgcg_step(void* x, void* r, void* p, void* s, const void* w, double* sc,
+                                int first, int64_t n, int32_t tau, void* stream) {
+  EHYB_TRY {
+    auto st = static_cast<cudaStream_t>(stream);
+    cgcg_scalars_kernel<<<1, 1, 0, st>>>(sc, first);
+    const int g = int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)));
+    if (tau == 4)
+      cgcg_update_kernel<float><<<g, 256, 0, st>>>(
+          static_cast<float*>(x), static_cast<float*>(r), static_cast<float*>(p),
+          static_cast<float*>(s), static_cast<const float*>(w), sc, n);
+    else
+      cgcg_update_kernel<double><<<g, 256, 0, st>>>(
+          static_cast<double*>(x), static_cast<double*>(r), static_cast<double*>(p),
+          static_cast<double*>(s), static_cast<const double*>(w), sc, n);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  EHYB_CATCH
+}
+
 EHYB_API int ehyb_dev_axpy(const double* a_dev, double sign, const void* x, void* y, int64_t n,
                            int32_t tau, void* stream) {
   EHYB_TRY {

@@ -28,6 +28,9 @@
 namespace ehyb {
 
 constexpr int kUnroll = 8;        // slots per lane in flight
+#ifndef EHYB_POOL_BATCH_F64
+#define EHYB_POOL_BATCH_F64 1
+#endif
 #ifndef EHYB_MAX_THREADS
 #define EHYB_MAX_THREADS 1024
 #endif
@@ -643,20 +646,45 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     if (lane == 0) v = atomicAdd(ctr, 1u);
     return P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
   };
+  // counts are published in batches of up to 4 slices: one gpu-scope fence
+  // per batch orders all their sums before the counter increments
+  // fp64 keeps the batch small: its ER slices need more registers
+  constexpr int kBatch = sizeof(T) == 4 ? 4 : EHYB_POOL_BATCH_F64;
+  uint32_t pend0 = 0, pend1 = 0, pend2 = 0, pend3 = 0;  // owners of unpublished slices
+  int n_pend = 0;
+  auto flush = [&]() {
+    if (n_pend == 0) return;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      atomicAdd(done + pend0, 1u);
+      if (n_pend > 1) atomicAdd(done + pend1, 1u);
+      if (n_pend > 2) atomicAdd(done + pend2, 1u);
+      if (n_pend > 3) atomicAdd(done + pend3, 1u);
+    }
+    n_pend = 0;
+  };
   auto finish = [&](int64_t s, const ErMeta& m) {
     const T acc = er_slice_compute<T, STRICT>(P, m);
     P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc;
-    __threadfence();
-    __syncwarp();
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
-    if (lane == 0) atomicAdd(done + uint32_t(rw0 & kRowMask) / uint32_t(P.vec), 1u);
+    const uint32_t owner = uint32_t(rw0 & kRowMask) / uint32_t(P.vec);
+    if (n_pend == 0) pend0 = owner;
+    else if (n_pend == 1) pend1 = owner;
+    else if (n_pend == 2) pend2 = owner;
+    else pend3 = owner;
+    if (++n_pend == kBatch) flush();
   };
   if (max_items > 0) {
     for (int i = 0; i < max_items; ++i) {
       const int64_t s = pclaim();
-      if (s >= P.pool_hi) return false;
+      if (s >= P.pool_hi) {
+        flush();
+        return false;
+      }
       finish(s, er_claimed_meta(P, s, P.pool_hi, lane));
     }
+    flush();
     return true;
   }
   int64_t s = pclaim();
@@ -668,6 +696,7 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     s = nxt;
     m = mn;
   }
+  flush();
   return false;
 }
 
@@ -1121,9 +1150,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     if (q1 > q0) {
       const unsigned int* done =
           P.pool_done + (ep & 1u) * uint32_t(P.n_parts) + uint32_t(part);
-      while (ld_acquire_gpu(done) != unsigned(q1 - q0)) {
-        if (!pool_drain<T, STRICT>(P, lane, 1, ep)) __nanosleep(128);  // help, else wait
-      }
+      // every pooled slice is claimed by now (this warp drained the pool
+      // above), so only slices still in flight elsewhere remain
+      while (ld_acquire_gpu(done) != unsigned(q1 - q0)) __nanosleep(128);
       for (int64_t idx = claim(&next_pcomb); idx < q1 - q0; idx = claim(&next_pcomb)) {
         const int64_t sl = __ldg(P.pool_own_idx + q0 + idx);
         const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
@@ -1250,6 +1279,110 @@ __global__ void cg_p_kernel(T* __restrict__ p, const T* __restrict__ r,
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     p[i] = r[i] + beta * p[i];
+}
+
+// Two dot products in one pass (Chronopoulos-Gear CG needs (r,r) and (w,r)
+// together): block partials, reduced by dot2_final_kernel.
+template <typename T>
+__global__ void dot2_partial_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                    const T* __restrict__ c, const T* __restrict__ d, int64_t n,
+                                    double* __restrict__ partial) {
+  __shared__ double red[2][32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    s0 += double(a[i]) * double(b[i]);
+    s1 += double(c[i]) * double(d[i]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s0;
+    red[1][threadIdx.x >> 5] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const bool ok = threadIdx.x < (blockDim.x >> 5);
+    s0 = ok ? red[0][threadIdx.x] : 0.0;
+    s1 = ok ? red[1][threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = s0;
+      partial[2 * blockIdx.x + 1] = s1;
+    }
+  }
+}
+
+__global__ void dot2_final_kernel(const double* __restrict__ partial, int n,
+                                  double* __restrict__ out) {
+  __shared__ double red[2][32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    s0 += partial[2 * i];
+    s1 += partial[2 * i + 1];
+  }
+  for (int o = 16; o; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s0;
+    red[1][threadIdx.x >> 5] = s1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const bool ok = threadIdx.x < (blockDim.x >> 5);
+    s0 = ok ? red[0][threadIdx.x] : 0.0;
+    s1 = ok ? red[1][threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (threadIdx.x == 0) {
+      out[0] = s0;
+      out[1] = s1;
+    }
+  }
+}
+
+// Chronopoulos-Gear CG scalars, kept on the device. sc = {gamma = (r,r),
+// delta = (w,r) (both all-reduced), gamma_old, alpha, beta}:
+// first iteration beta = 0, alpha = gamma/delta; then beta = gamma/gamma_old,
+// alpha = gamma / (delta - beta*gamma/alpha_old).
+__global__ void cgcg_scalars_kernel(double* __restrict__ sc, int first) {
+  const double g = sc[0], d = sc[1];
+  double beta = 0.0, alpha;
+  if (first) {
+    alpha = g / d;
+  } else {
+    beta = g / sc[2];
+    alpha = g / (d - beta * g / sc[3]);
+  }
+  sc[2] = g;
+  sc[3] = alpha;
+  sc[4] = beta;
+}
+
+// p = r + beta p; s = w + beta s; x += alpha p; r -= alpha s
+template <typename T>
+__global__ void cgcg_update_kernel(T* __restrict__ x, T* __restrict__ r, T* __restrict__ p,
+                                   T* __restrict__ s, const T* __restrict__ w,
+                                   const double* __restrict__ sc, int64_t n) {
+  const T alpha = T(sc[3]), beta = T(sc[4]);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T pi = r[i] + beta * p[i];
+    const T si = w[i] + beta * s[i];
+    p[i] = pi;
+    s[i] = si;
+    x[i] = x[i] + alpha * pi;
+    r[i] = r[i] - alpha * si;
+  }
 }
 
 template <typename T>

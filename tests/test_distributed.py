@@ -130,7 +130,8 @@ def test_shards_on_one_gpu_bitwise(world, tau):
 
 
 @pytest.mark.gpu
-def test_cg_converges_single_gpu():
+@pytest.mark.parametrize("method", ["chronopoulos-gear", "classic"])
+def test_cg_converges_single_gpu(method):
     m, e = matrix()
     plan = D.plan_for(e, 0, 1)
     A = D.DistributedEhyb(e, device=0, plan=plan)
@@ -139,7 +140,8 @@ def test_cg_converges_single_gpu():
     # padding rows of b stay 0 (empty rows), so the solution there is 0
     b = torch.empty(A.local_rows, dtype=torch.float64, device="cuda:0")
     A.spmv_local(ones, b)
-    x, info = D.cg(A, b, maxiter=200, tol=1e-10)
+    x, info = D.cg(A, b, maxiter=200, tol=1e-10, method=method)
+    assert info["method"] == method
     torch.cuda.synchronize()
     real = np.zeros(A.local_rows, bool)
     real[e.plan.reorder_table[: e.dimension]] = True
