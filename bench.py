@@ -330,9 +330,10 @@ def run_gpu(args):
         times = []
         for _ in range(6):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            g.replay()
-            b.record(stream)
+            with torch.cuda.stream(stream):  # replay runs on the current stream
+                a.record(stream)
+                g.replay()
+                b.record(stream)
             b.synchronize()
             times.append(a.elapsed_time(b) / 1e3 / R)
         t_graph = statistics.median(times[1:])

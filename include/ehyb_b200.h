@@ -214,7 +214,7 @@ EHYB_API int ehyb_dev_spmv_host(ehyb_dev* h, const void* x_host, void* y_host, i
 
 /* A sequence of independent products from HOST memory (the same call as
  * ehyb_dev_spmv_host repeated `count` times: vector i is x_hosts[i] ->
- * y_hosts[i], user_order as above), pipelined on two device buffer pairs:
+ * y_hosts[i], user_order as above), pipelined on three device buffer pairs:
  * the copy-in of vector i+1 and the copy-out of vector i-1 overlap the
  * product of vector i (copy-in / copy-out on handle-owned streams, compute on
  * `stream`). Returns after the last copy-out; host buffers should be pinned.
@@ -251,9 +251,13 @@ typedef struct ehyb_shard_plan {
 EHYB_API int ehyb_dev_create_shard(const ehyb_host_matrix* m, const ehyb_shard_plan* plan,
                                    int device, ehyb_dev** out);
 
-/* Split SpMV for overlap with the halo exchange: the ELL phase needs only
- * owned x; the ER phase needs x_ext complete. ehyb_dev_spmv on a shard
- * handle runs both back to back. */
+/* Split SpMV for overlap with the halo exchange.
+ * ehyb_dev_spmv_ell: the local phase — ELL plus every ER row whose columns
+ *   are all owned (own slices, shared-memory buffer, cross-CTA pool); reads
+ *   only x_ext[0, local_rows), so it runs while the halo is in flight.
+ * ehyb_dev_spmv_er: the halo phase — ER rows with a halo column and long
+ *   rows; needs x_ext complete. Each ER row is added to y exactly once.
+ * ehyb_dev_spmv on a shard handle runs all of it in one launch. */
 EHYB_API int ehyb_dev_spmv_ell(ehyb_dev* h, const void* x_ext, void* y_local, int mode,
                                void* stream);
 EHYB_API int ehyb_dev_spmv_er(ehyb_dev* h, const void* x_ext, void* y_local, int mode,

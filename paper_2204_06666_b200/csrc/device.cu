@@ -85,6 +85,7 @@ struct ehyb_dev {
   // derived ER
   int64_t er_slices = 0, er_slots = 0;
   int32_t* er_part_ptr = nullptr;
+  int32_t* er_part_mid = nullptr;  // first halo slice of each partition (shards)
   int64_t* er_pos = nullptr;
   int32_t* er_swidth = nullptr;
   int32_t* er_rows = nullptr;
@@ -145,22 +146,23 @@ struct ehyb_dev {
   unsigned int* lr_ctr = nullptr;
   // host-batch pipeline (ehyb_dev_spmv_host_many): copy-in / copy-out streams,
   // two device buffer pairs, per-buffer events
+  static constexpr int kPipe = 3;  // device buffer pairs in flight
   cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
-              ev_out[2] = {nullptr, nullptr};
-  void* bx[2] = {nullptr, nullptr};
-  void* by[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[kPipe] = {}, ev_comp[kPipe] = {}, ev_out[kPipe] = {};
+  void* bx[kPipe] = {};
+  void* by[kPipe] = {};
 
   ~ehyb_dev() {
-    void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_pos, er_swidth,
+    void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
                     pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev,
-                    part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage, bx[0], bx[1], by[0], by[1], long_bits, lr_span,
+                    part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
+                    bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
                     lr_part, lr_cnt, lr_ctr};
     for (void* p : ptrs)
       if (p) cudaFree(p);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kPipe; ++b) {
       if (ev_in[b]) cudaEventDestroy(ev_in[b]);
       if (ev_comp[b]) cudaEventDestroy(ev_comp[b]);
       if (ev_out[b]) cudaEventDestroy(ev_out[b]);
@@ -181,6 +183,12 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pos_ell = h->pos_ell;
   P.width_ell = h->width_ell;
   P.er_part_ptr = h->er_part_ptr;
+  P.er_part_mid = h->er_part_mid;
+  // launch kinds: full (ELL + all ER), local phase (ELL + ER rows whose columns
+  // are all owned, pool included), halo phase (ER rows with a halo column and
+  // long rows, after the exchange)
+  P.er_sel = (do_ell && do_er) ? 0 : (do_ell ? 1 : 2);
+  do_er = true;
   P.er_pos = h->er_pos;
   P.er_swidth = h->er_swidth;
   P.er_rows = h->er_rows;
@@ -227,6 +235,11 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.lr_part = static_cast<T*>(h->lr_part);
   P.lr_cnt = h->lr_cnt;
   P.lr_ctr = h->lr_ctr;
+  if (P.er_sel == 1) P.lr_tasks = 0;  // long rows may read the halo: halo phase
+  if (P.er_sel == 2) {                 // the pool holds local rows only
+    P.pool_lo = P.pool_hi;
+    P.pool_own_ptr = nullptr;
+  }
   void (*kern)(const SpmvParams<T>) = (do_ell && h->window_in_smem)
                                            ? spmv_fused_kernel<T, STRICT, C32, true, false>
                                            : spmv_fused_kernel<T, STRICT, C32, false, false>;
@@ -441,11 +454,24 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
 
   // ---- ER regrouped per owning partition
   const int64_t n_loc_parts = p1 - p0;
-  std::vector<std::vector<int64_t>> members(static_cast<size_t>(n_loc_parts));
+  // shards: rows with a column outside the shard ("halo rows") form their own
+  // slices, run by the halo launch after the exchange; all other ER rows run
+  // in the first launch together with ELL
+  std::vector<std::vector<int64_t>> members(static_cast<size_t>(n_loc_parts)),
+      hmembers(static_cast<size_t>(n_loc_parts));
   for (int64_t j = 0; j < m->n_er_rows; ++j) {
     const int64_t r = m->y_idx_er[j];
-    if (r >= row_lo && r < row_hi && !((lbits[size_t((r - row_lo) >> 5)] >> ((r - row_lo) & 31)) & 1u))
-      members[size_t(r / vec - p0)].push_back(j);
+    if (r < row_lo || r >= row_hi || ((lbits[size_t((r - row_lo) >> 5)] >> ((r - row_lo) & 31)) & 1u))
+      continue;
+    bool halo = false;
+    if (shard) {
+      const int64_t src0 = int64_t(m->position_er[j / C]) + j % C;
+      for (int64_t k = 0; k < m->er_row_widths[j] && !halo; ++k) {
+        const int64_t c = m->col_er[src0 + C * k];
+        halo = c < row_lo || c >= row_hi;
+      }
+    }
+    (halo ? hmembers : members)[size_t(r / vec - p0)].push_back(j);
   }
   std::unordered_map<int64_t, int64_t> halo_index;
   halo_index.reserve(size_t(n_halo) * 2 + 1);
@@ -490,7 +516,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     total += ell_cost[size_t(q)] + er_total[size_t(q)];
   }
   const double budget_mean = n_loc_parts ? total / double(n_loc_parts) : 0.0;
-  struct SliceRef { int64_t q, i0; };
+  struct SliceRef { int64_t q, i0; bool halo; };
   std::vector<std::vector<SliceRef>> own(static_cast<size_t>(n_loc_parts)), spill(static_cast<size_t>(n_loc_parts));
   for (int64_t q = 0; q < n_loc_parts; ++q) {
     const auto& mem = members[size_t(q)];
@@ -502,17 +528,19 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       for (size_t i = i0; i < std::min(mem.size(), i0 + 32); ++i) c += er_cost * m->er_row_widths[mem[i]];
       if (!spilling && c <= left) {
         left -= c;
-        own[size_t(q)].push_back({q, int64_t(i0)});
+        own[size_t(q)].push_back({q, int64_t(i0), false});
       } else {
         spilling = true;
-        spill[size_t(q)].push_back({q, int64_t(i0)});
+        spill[size_t(q)].push_back({q, int64_t(i0), false});
       }
     }
   }
-  std::vector<int32_t> part_ptr(size_t(n_loc_parts) + 1, 0);
+  std::vector<int32_t> part_ptr(size_t(n_loc_parts) + 1, 0), part_mid(static_cast<size_t>(n_loc_parts), 0);
   std::vector<SliceRef> order;
   for (int64_t q = 0; q < n_loc_parts; ++q) {
     for (const auto& r : own[size_t(q)]) order.push_back(r);
+    part_mid[size_t(q)] = int32_t(order.size());
+    for (size_t i0 = 0; i0 < hmembers[size_t(q)].size(); i0 += 32) order.push_back({q, int64_t(i0), true});
     part_ptr[size_t(q) + 1] = int32_t(order.size());
   }
   h->pool_lo = int64_t(order.size());
@@ -623,7 +651,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       elwidth(size_t(n_sl) * 32, 0);
   for (int64_t sl = 0; sl < n_sl; ++sl) {
     const auto& ref = order[size_t(sl)];
-    const auto& mem = members[size_t(ref.q)];
+    const auto& mem = ref.halo ? hmembers[size_t(ref.q)] : members[size_t(ref.q)];
     for (int64_t i = ref.i0; i < std::min<int64_t>(int64_t(mem.size()), ref.i0 + 32); ++i) {
       const int64_t j = mem[size_t(i)];
       const int32_t w = m->er_row_widths[j];
@@ -642,7 +670,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::vector<uint32_t> ecols(size_t(std::max<int64_t>(eslots, 1)), 0);
   for (int64_t sl = 0; sl < n_sl; ++sl) {
     const auto& ref = order[size_t(sl)];
-    const auto& mem = members[size_t(ref.q)];
+    const auto& mem = ref.halo ? hmembers[size_t(ref.q)] : members[size_t(ref.q)];
     for (int64_t i = ref.i0; i < std::min<int64_t>(int64_t(mem.size()), ref.i0 + 32); ++i) {
       const int64_t j = mem[size_t(i)];
       const int64_t w = m->er_row_widths[j];
@@ -667,6 +695,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->er_slices = n_sl;
   h->er_slots = eslots;
   CUDA_TRY(upload(&h->er_part_ptr, part_ptr.data(), part_ptr.size() * 4, &h->bytes));
+  CUDA_TRY(upload(&h->er_part_mid, part_mid.data(), part_mid.size() * 4, &h->bytes));
   CUDA_TRY(upload(&h->er_pos, epos.data(), epos.size() * 8, &h->bytes));
   CUDA_TRY(upload(&h->er_swidth, eswidth.data(), eswidth.size() * 4, &h->bytes));
   CUDA_TRY(upload(&h->er_rows, erows.data(), erows.size() * 4, &h->bytes));
@@ -997,14 +1026,14 @@ EHYB_API int ehyb_dev_spmv_host(ehyb_dev* h, const void* x_host, void* y_host, i
 static int ensure_pipeline(ehyb_dev* h) {
   if (h->s_in) return 0;
   const size_t pb = size_t(h->padded) * size_t(h->tau);
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < ehyb_dev::kPipe; ++b) {
     CUDA_TRY(cudaMalloc(&h->bx[b], pb));
     CUDA_TRY(cudaMalloc(&h->by[b], pb));
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_comp[b], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming));
   }
-  h->bytes += 4 * pb;
+  h->bytes += 2 * ehyb_dev::kPipe * pb;
   CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
   return 0;
@@ -1029,15 +1058,16 @@ EHYB_API int ehyb_dev_spmv_host_many(ehyb_dev* h, const void* const* x_hosts,
     cudaEvent_t ev_start = h->ev_out[0];
     CUDA_TRY(cudaEventRecord(ev_start, st));
     CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
+    constexpr int K = ehyb_dev::kPipe;
     for (int64_t i = 0; i < count; ++i) {
-      const int b = int(i & 1);
-      // copy-in: buffer b is free once the compute of vector i-2 has read it
-      if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_comp[b], 0));
+      const int b = int(i % K);
+      // copy-in: buffer b is free once the compute of vector i-K has read it
+      if (i >= K) CUDA_TRY(cudaStreamWaitEvent(h->s_in, h->ev_comp[b], 0));
       CUDA_TRY(cudaMemcpyAsync(h->bx[b], x_hosts[i], nb, cudaMemcpyHostToDevice, h->s_in));
       CUDA_TRY(cudaEventRecord(h->ev_in[b], h->s_in));
-      // compute on the caller's stream; by[b] is free once the copy-out of i-2 ended
+      // compute on the caller's stream; by[b] is free once the copy-out of i-K ended
       CUDA_TRY(cudaStreamWaitEvent(st, h->ev_in[b], 0));
-      if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_out[b], 0));
+      if (i >= K) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_out[b], 0));
       if (user_order) {
         rc = ehyb_dev_spmv_user(h, h->bx[b], h->by[b], mode, stream);
         if (rc) return rc;

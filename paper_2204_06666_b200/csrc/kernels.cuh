@@ -46,6 +46,8 @@ struct SpmvParams {
   const int32_t* __restrict__ width_ell;
   // derived per-partition ER (32-row SELL slices)
   const int32_t* __restrict__ er_part_ptr;  // [n_parts+1] slice ranges
+  const int32_t* __restrict__ er_part_mid;  // [n_parts] first slice with a halo column (shards)
+  int32_t er_sel;                           // 0: all own slices, 1: [ptr, mid), 2: [mid, ptr+1)
   const int64_t* __restrict__ er_pos;       // [n_slices] slot offset of each slice
   const int32_t* __restrict__ er_swidth;    // [n_slices] slice width
   const int32_t* __restrict__ er_rows;      // [n_slices*32] row | kPadFlag, -1 = empty lane
@@ -772,8 +774,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   for (int it = 0, part = cta; part < P.n_parts; ++it, part += gridDim.x) {
   const int64_t row0 = int64_t(part) * P.vec;
   const T* xwin = P.x + row0;
-  const int64_t s0 = __ldg(P.er_part_ptr + part);
-  const int64_t s1 = __ldg(P.er_part_ptr + part + 1);
+  const int64_t s0 = P.er_sel == 2 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part);
+  const int64_t s1 = P.er_sel == 1 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part + 1);
   const uint32_t phase = uint32_t(it) & 1u;
 
   if (it > 0) __syncthreads();  // every warp is done with the previous partition

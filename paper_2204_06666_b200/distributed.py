@@ -8,8 +8,11 @@ reference their own partition's window). Owned ER rows reference remote
 columns; the halo plan lists them per peer once, and every SpMV exchanges
 exactly those values with one NCCL all-to-all that overlaps the ELL launch:
 
-    pack (gather kernel) -> all_to_all_single (async)  ||  ELL-only launch
-                         -> wait -> ER-only launch
+    pack (gather kernel) -> all_to_all_single (async)  ||  local launch
+                         -> wait -> halo launch
+
+The local launch runs ELL and every ER row whose columns are all owned; the
+halo launch only the ER rows that read a halo column (and long rows).
 
 `x_ext = [owned x (local_rows) | halo (n_halo)]`; the derived ER columns of
 the shard are remapped into that space at upload (ehyb_dev_create_shard).
@@ -21,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import time
 import weakref
 from dataclasses import dataclass
@@ -389,7 +393,19 @@ def bench_main(args, clock_cls=None):
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    # the driver parses one JSON line from stdout: keep NCCL's banner off it
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist.barrier()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     path = os.path.join(os.environ.get("EHYB_SCRATCH", "/tmp"), f"ehyb_weak_{world}.ehyb")
     t0 = time.perf_counter()
     nnz = None

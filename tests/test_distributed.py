@@ -108,11 +108,25 @@ def test_plans_are_consistent():
         assert sum(p.local_rows for p in plans) == e.padded_dimension
 
 
+def heavy_matrix(tau=8):
+    n, r, c, v = W.heavy_tail(k=14, n_hubs=4, min_len=100, max_len=1500)
+    m = E.CooMatrix(n, n, r, c, v)
+    return m, E.build_ehyb(m, tau=tau, profile=E.DeviceProfile(12, 32, 8192))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [1, 2, 3])
 @pytest.mark.parametrize("tau", [4, 8])
-def test_shards_on_one_gpu_bitwise(world, tau):
-    m, e = matrix(tau)
+@pytest.mark.parametrize("kind", ["stencil", "heavy"])
+def test_shards_on_one_gpu_bitwise(world, tau, kind, monkeypatch):
+    # local launch (ELL + ER rows with owned columns) then halo launch (ER
+    # rows with a halo column, long rows), and the single fused launch:
+    # both bitwise equal to the full product
+    if kind == "heavy":
+        monkeypatch.setenv("EHYB_LONG_ROW", "40")
+        m, e = heavy_matrix(tau)
+    else:
+        m, e = matrix(tau)
     xr = E.permute_vector(W.deterministic_vector(e.dimension, 0), e.plan)
     y_full, _ = E.spmv_ehyb(e, xr)
     dt = torch.float32 if tau == 4 else torch.float64
@@ -127,6 +141,13 @@ def test_shards_on_one_gpu_bitwise(world, tau):
         A.spmv_local(x_ext, y)
         torch.cuda.synchronize()
         assert y.cpu().numpy().tobytes() == y_full[lo:hi].tobytes()
+        y2 = torch.empty_like(y)
+        import ctypes as C
+        from paper_2204_06666_b200 import _lib as L
+        L.call("ehyb_dev_spmv", A._h, C.c_void_p(x_ext.data_ptr()), C.c_void_p(y2.data_ptr()),
+               L.MODE_STRICT, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert y2.cpu().numpy().tobytes() == y_full[lo:hi].tobytes()
 
 
 @pytest.mark.gpu
