@@ -117,6 +117,7 @@ struct ehyb_dev {
   int32_t* pool_own_ptr = nullptr;
   int32_t* pool_own_idx = nullptr;
   void* pool_acc = nullptr;
+  unsigned int* cta_flag = nullptr;  // [max_ctas] persistent-mode publication
   unsigned int* pool_ctr = nullptr;
   unsigned int* epoch_dev = nullptr;  // [2] launch epoch, CTAs finished (device-side: graph-safe)
   // own-ER shared-memory buffer
@@ -155,7 +156,7 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev,
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev, cta_flag,
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
@@ -213,6 +214,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_own_ptr = h->pool_own_ptr;
   P.pool_own_idx = h->pool_own_idx;
   P.pool_acc = static_cast<T*>(h->pool_acc);
+  P.cta_flag = h->cta_flag;
   P.epoch_dev = h->epoch_dev;
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
@@ -285,6 +287,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   // at most one wave of resident CTAs; each loops over its partitions
   const int64_t n_local_parts = h->local_rows / h->vec;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(n_local_parts, h->max_ctas));
+
   kern<<<dim3(unsigned(grid)), dim3(unsigned(h->threads)), smem, st>>>(P);
   return cudaGetLastError();
 }
@@ -823,6 +826,11 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(cudaMalloc(&h->pool_ctr, 16));
     CUDA_TRY(cudaMemset(h->pool_ctr, 0, 16));
     h->bytes += acc_bytes + size_t(n_loc_parts) * 8 + 32;
+    if (n_loc_parts > h->max_ctas && env_double("EHYB_POOL_DIRECT", 1.0) != 0.0) {
+      CUDA_TRY(cudaMalloc(&h->cta_flag, size_t(h->max_ctas) * 4 + 16));
+      CUDA_TRY(cudaMemset(h->cta_flag, 0, size_t(h->max_ctas) * 4 + 16));
+      h->bytes += size_t(h->max_ctas) * 4 + 16;
+    }
   }
   *out = h.release();
   return 0;

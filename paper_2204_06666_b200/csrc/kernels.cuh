@@ -75,6 +75,7 @@ struct SpmvParams {
   const int32_t* __restrict__ pool_own_ptr;  // [n_parts+1] pooled slices of each partition
   const int32_t* __restrict__ pool_own_idx;  // their slice indices
   T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
+  unsigned int* cta_flag;           // [grid] epoch in which a CTA finished all its partitions
   unsigned int* epoch_dev;          // [2]: launch sequence number (>= 1), CTAs finished; kept
                                     // on the device so a captured CUDA graph replays correctly
   // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
@@ -487,6 +488,52 @@ __device__ __forceinline__ T er_slice_compute(const SpmvParams<T>& P, const ErMe
   return acc;
 }
 
+#ifndef EHYB_ER_PAIRS
+#define EHYB_ER_PAIRS 1
+#endif
+// Two ER slices at once (one warp, lane = row in each): their loads and x
+// gathers are issued together, so a latency-bound slice costs half the warp
+// time. b may be an empty claim (rw = -1, widths 0). Per row the order is the
+// reference's k order; the padding products as in er_slice_compute.
+template <typename T, bool STRICT>
+__device__ __forceinline__ void er_pair_compute(const SpmvParams<T>& P, const ErMeta& a,
+                                                const ErMeta& b, T& acc_a, T& acc_b) {
+  constexpr int U = 4;
+  acc_a = T(0);
+  acc_b = T(0);
+  const int sw = a.sw > b.sw ? a.sw : b.sw;
+  for (int k = 0; k < sw; k += U) {
+    T va[U], vb[U];
+    uint32_t ca[U], cb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ca[u] = cb[u] = 0;
+      va[u] = vb[u] = T(0);
+      if (k + u < a.lw) {
+        ca[u] = __ldcs(P.er_col + a.pos + int64_t(k + u) * 32);
+        va[u] = __ldcs(P.er_val + a.pos + int64_t(k + u) * 32);
+      }
+      if (k + u < b.lw) {
+        cb[u] = __ldcs(P.er_col + b.pos + int64_t(k + u) * 32);
+        vb[u] = __ldcs(P.er_val + b.pos + int64_t(k + u) * 32);
+      }
+    }
+    T xa[U], xb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      xa[u] = (k + u < a.lw) ? __ldg(P.x + ca[u]) : T(0);
+      xb[u] = (k + u < b.lw) ? __ldg(P.x + cb[u]) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k + u < a.lw) acc_a = madd<STRICT>(acc_a, va[u], xa[u]);
+      if (k + u < b.lw) acc_b = madd<STRICT>(acc_b, vb[u], xb[u]);
+    }
+  }
+  if (a.rw >= 0 && (a.rw & kPadFlag)) acc_a = add_rn(acc_a, mul_rn(T(0), __ldg(P.x)));
+  if (b.rw >= 0 && (b.rw & kPadFlag)) acc_b = add_rn(acc_b, mul_rn(T(0), __ldg(P.x)));
+}
+
 // ------------------------------------------------------------- long rows
 // STRICT: the reference's serial order over entries [lo, hi) — acc from +0.0,
 // each product rounded, then added. Entries are fetched 32*LB at a time (lane
@@ -689,6 +736,28 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     flush();
     return true;
   }
+  if constexpr (EHYB_ER_PAIRS && sizeof(T) == 4) {
+  for (;;) {  // two slices per claim (fp32: the pair fits the register budget)
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 2u);
+    const int64_t s = P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
+    if (s >= P.pool_hi) break;
+    const bool two = s + 1 < P.pool_hi;
+    const ErMeta ma = er_claimed_meta(P, s, P.pool_hi, lane);
+    const ErMeta mb = er_claimed_meta(P, s + 1, P.pool_hi, lane);
+    T acc_a, acc_b;
+    er_pair_compute<T, STRICT>(P, ma, mb, acc_a, acc_b);
+    P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc_a;
+    if (two) P.pool_acc[(s + 1 - P.pool_lo) * 32 + lane] = acc_b;
+    __threadfence();
+    __syncwarp();
+    const int32_t ra = __shfl_sync(0xffffffffu, ma.rw, 0), rb = __shfl_sync(0xffffffffu, mb.rw, 0);
+    if (lane == 0) {
+      atomicAdd(done + uint32_t(ra & kRowMask) / uint32_t(P.vec), 1u);
+      if (two) atomicAdd(done + uint32_t(rb & kRowMask) / uint32_t(P.vec), 1u);
+    }
+  }
+  } else {
   int64_t s = pclaim();
   ErMeta m = er_claimed_meta(P, s, P.pool_hi, lane);
   while (s < P.pool_hi) {  // next slice's metadata one claim ahead
@@ -698,8 +767,44 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     s = nxt;
     m = mn;
   }
+}
   flush();
   return false;
+}
+
+// Pooled ER slices when CTAs run several partitions: drained after the
+// CTA's own partitions, two per claim, each row finished in place as
+// y[r] = y_ell[r] + sum once the CTA owning r has published all its
+// partitions (cta_flag == epoch). Publishing never waits on the pool, so the
+// waits always end.
+template <typename T, bool STRICT>
+__device__ void pool_drain_direct(const SpmvParams<T>& P, int lane, uint32_t ep) {
+  if (P.pool_hi <= P.pool_lo) return;
+  unsigned int* ctr = P.pool_ctr + (ep & 1u);
+  auto finish = [&](const ErMeta& m, T acc) {
+    if (m.rw < 0) return;
+    const uint32_t r = uint32_t(m.rw & kRowMask);
+    const uint32_t owner = (r / uint32_t(P.vec)) % gridDim.x;
+    while (ld_acquire_gpu(P.cta_flag + owner) != ep) __nanosleep(64);
+    P.y[r] = add_rn(__ldcg(P.y + r), acc);
+  };
+  constexpr unsigned kStep = (EHYB_ER_PAIRS && sizeof(T) == 4) ? 2u : 1u;
+  for (;;) {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, kStep);
+    const int64_t s = P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
+    if (s >= P.pool_hi) break;
+    const ErMeta ma = er_claimed_meta(P, s, P.pool_hi, lane);
+    if constexpr (kStep == 2u) {
+      const ErMeta mb = er_claimed_meta(P, s + 1, P.pool_hi, lane);
+      T acc_a, acc_b;
+      er_pair_compute<T, STRICT>(P, ma, mb, acc_a, acc_b);
+      finish(ma, acc_a);
+      finish(mb, acc_b);
+    } else {
+      finish(ma, er_slice_compute<T, STRICT>(P, ma));
+    }
+  }
 }
 
 __device__ __forceinline__ int lds_volatile(const uint32_t* p, uint32_t bit) {
@@ -763,6 +868,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   }
   __syncthreads();
   const uint32_t ep = s_ep;
+  const bool persistent = int(gridDim.x) < P.n_parts;
+  auto claim = [&](int* ctr) -> int64_t {
+    int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
   // ring producer state (lane 0 of the last warp), kept across partitions
   const int prod_warp = int(blockDim.x >> 5) - 1;
   int64_t r_sbase = 0;  // stages of this CTA's earlier partitions (ring stage numbering)
@@ -843,11 +954,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   const int64_t n_buf = (P.do_er && P.do_ell) ? (n_own < P.er_buf_slices ? n_own : P.er_buf_slices) : 0;
   T* er_buf = reinterpret_cast<T*>(smem_raw + P.er_buf_offset);
 
-  auto claim = [&](int* ctr) -> int64_t {
-    int v = 0;
-    if (lane == 0) v = atomicAdd(ctr, 1);
-    return __shfl_sync(0xffffffffu, v, 0);
-  };
   auto wait_chunk = [&](int64_t r) {
     const int64_t ch = (r - row0) >> 5;
     const uint32_t bit = 1u << (ch & 31);
@@ -949,14 +1055,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     unpublished = chunk;
   };
   auto er_meta = [&](int64_t s, int64_t s_end) { return er_claimed_meta(P, s, s_end, lane); };
-  auto finish_own_er = [&](int64_t idx, const ErMeta& m) {
-    // a row whose ELL value is already final has y read before the slice's
-    // loads, so that round trip overlaps them
+  // a row whose ELL value is already final has y read before the slice's
+  // loads, so that round trip overlaps them
+  auto own_pre = [&](int64_t idx, const ErMeta& m, T& yv) -> bool {
     const bool direct = idx >= n_buf && m.rw >= 0;
-    const int64_t r = m.rw & kRowMask;
     bool have_y = false;
-    T yv = T(0);
     if (direct) {
+      const int64_t r = m.rw & kRowMask;
       if (!P.do_ell) {
         have_y = true;
       } else {
@@ -968,6 +1073,28 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       }
       if (have_y) yv = __ldcg(P.y + r);
     }
+    return have_y;
+  };
+  auto own_post = [&](int64_t idx, const ErMeta& m, T acc, T yv, bool have_y) {
+    if (idx < n_buf) {
+      er_buf[idx * 32 + lane] = acc;
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) atomicOr(&er_done[idx >> 5], 1u << (idx & 31));
+    } else if (m.rw >= 0) {
+      const int64_t r = m.rw & kRowMask;
+      if (!have_y) {
+        wait_chunk(r);
+        yv = __ldcg(P.y + r);
+      }
+      P.y[r] = add_rn(yv, acc);
+    }
+  };
+  auto finish_own_er = [&](int64_t idx, const ErMeta& m) {
+    const bool direct = idx >= n_buf && m.rw >= 0;
+    const int64_t r = m.rw & kRowMask;
+    T yv = T(0);
+    const bool have_y = own_pre(idx, m, yv);
     const T acc = er_slice_compute<T, STRICT>(P, m);
     if (idx < n_buf) {
       er_buf[idx * 32 + lane] = acc;
@@ -995,8 +1122,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
         finish_own_er(idx, er_meta(s0 + idx, s1));
       }
     }
-    // pooled slices of every partition, hidden behind the other warps' ELL stream
-    pool_drain<T, STRICT>(P, lane, 0, ep);
+    // pooled slices of every partition, hidden behind the other warps' ELL
+    // stream (a CTA running several partitions drains the pool after them)
+    if (!persistent) pool_drain<T, STRICT>(P, lane, 0, ep);
   }
   const int64_t st_lo = RING ? int64_t(__ldg(P.part_stage_ptr + part)) : 0;
   const int64_t n_st = RING ? int64_t(__ldg(P.part_stage_ptr + part + 1)) - st_lo : 0;
@@ -1113,7 +1241,22 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
 
   if (P.do_er) {
     if (pending >= 0 && pending < n_own) finish_own_er(pending, er_meta(s0 + pending, s1));
-    if (P.er_ahead) {
+    if constexpr (EHYB_ER_PAIRS && sizeof(T) == 4) {
+    for (;;) {  // two own slices per claim (fp32: the pair fits the register budget)
+      int v = 0;
+      if (lane == 0) v = atomicAdd(&next_er, 2);
+      const int64_t idx = __shfl_sync(0xffffffffu, v, 0);
+      if (idx >= n_own) break;
+      const ErMeta ma = er_meta(s0 + idx, s1), mb = er_meta(s0 + idx + 1, s1);
+      T ya = T(0), yb = T(0);
+      const bool ha = own_pre(idx, ma, ya);
+      const bool hb = idx + 1 < n_own ? own_pre(idx + 1, mb, yb) : false;
+      T acc_a, acc_b;
+      er_pair_compute<T, STRICT>(P, ma, mb, acc_a, acc_b);
+      own_post(idx, ma, acc_a, ya, ha);
+      if (idx + 1 < n_own) own_post(idx + 1, mb, acc_b, yb, hb);
+    }
+    } else if (P.er_ahead) {
       int64_t idx = claim(&next_er);
       ErMeta m = er_meta(s0 + idx, s1);
       while (idx < n_own) {
@@ -1127,12 +1270,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       for (int64_t idx = claim(&next_er); idx < n_own; idx = claim(&next_er))
         finish_own_er(idx, er_meta(s0 + idx, s1));
     }
+
     auto stamp = [&](int i) {
       if (P.timing && lane == 0 && !(RING && (i == 5 || i == 6)))
         atomicMax(P.timing + 8 * cta + i, globaltimer());
     };
     stamp(4);
-    pool_drain<T, STRICT>(P, lane, 0, ep);  // whatever the ER-first warps left
+    if (!persistent) pool_drain<T, STRICT>(P, lane, 0, ep);  // whatever the ER-first warps left
     // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
     for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
       while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
@@ -1147,8 +1291,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     }
     stamp(5);
     // pooled slices of this partition: once all are in, y[r] = y_ell[r] + sum
-    const int32_t q0 = P.pool_own_ptr ? __ldg(P.pool_own_ptr + part) : 0;
-    const int32_t q1 = P.pool_own_ptr ? __ldg(P.pool_own_ptr + part + 1) : 0;
+    // (a CTA that runs several partitions does this once, after all of them)
+    const int32_t q0 = (P.pool_own_ptr && !persistent) ? __ldg(P.pool_own_ptr + part) : 0;
+    const int32_t q1 = (P.pool_own_ptr && !persistent) ? __ldg(P.pool_own_ptr + part + 1) : 0;
     if (q1 > q0) {
       const unsigned int* done =
           P.pool_done + (ep & 1u) * uint32_t(P.n_parts) + uint32_t(part);
@@ -1169,6 +1314,41 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   }
   r_sbase += n_st;
   }  // partitions of this CTA
+
+  if (persistent && P.do_er && P.cta_flag) {
+    // several partitions per CTA: publish this CTA's rows, then drain the
+    // pool finishing rows in place (no scratch pass)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(P.cta_flag + cta, ep);
+    pool_drain_direct<T, STRICT>(P, lane, ep);
+  } else if (persistent && P.do_er && P.pool_own_ptr) {
+    pool_drain<T, STRICT>(P, lane, 0, ep);
+    __syncthreads();
+    for (int64_t t = claim(&next_pcomb);; t = claim(&next_pcomb)) {
+      int64_t base = 0;
+      int pt = -1;
+      int32_t q0 = 0, cnt = 0;
+      for (int p = cta; p < P.n_parts; p += gridDim.x) {
+        q0 = __ldg(P.pool_own_ptr + p);
+        cnt = __ldg(P.pool_own_ptr + p + 1) - q0;
+        if (t < base + cnt) {
+          pt = p;
+          break;
+        }
+        base += cnt;
+      }
+      if (pt < 0) break;
+      const unsigned int* done = P.pool_done + (ep & 1u) * uint32_t(P.n_parts) + uint32_t(pt);
+      while (ld_acquire_gpu(done) != unsigned(cnt)) __nanosleep(128);
+      const int64_t sl = __ldg(P.pool_own_idx + q0 + (t - base));
+      const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
+      if (rw >= 0) {
+        const int64_t r = rw & kRowMask;
+        P.y[r] = add_rn(__ldcg(P.y + r), __ldcg(P.pool_acc + (sl - P.pool_lo) * 32 + lane));
+      }
+    }
+  }
 
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -62,6 +62,98 @@ def halo_columns(e: EhybMatrix, p0: int, p1: int) -> np.ndarray:
     return np.unique(cols)
 
 
+def partition_quotient(e: EhybMatrix) -> np.ndarray:
+    """Dense n_parts x n_parts weights: ER entries of a row owned by partition
+    p that read a column of partition q (the traffic a p/q split would move)."""
+    vec, warp = e.params.vec_cache_size, e.params.warp_size
+    n_parts = e.n_parts
+    w = np.asarray(e.er_row_widths, np.int64)
+    slots = np.repeat(np.arange(w.size, dtype=np.int64), w)
+    k = np.arange(slots.size, dtype=np.int64) - np.repeat(np.cumsum(w) - w, w)
+    pos = np.asarray(e.position_er, np.int64)[slots // warp] + slots % warp + k * warp
+    src = np.asarray(e.plan.y_idx_er, np.int64)[slots] // vec
+    dst = np.asarray(e.col_er, np.int64)[pos] // vec
+    q = np.zeros((n_parts, n_parts), np.int64)
+    np.add.at(q, (src, dst), 1)
+    return q
+
+
+def group_partitions(e: EhybMatrix, world: int) -> np.ndarray:
+    """Partition order whose contiguous `part_range` blocks are compact in the
+    partition quotient graph: greedy graph growing — each
+    group starts from the unassigned partition with the least weight to other
+    unassigned ones and repeatedly takes the unassigned partition it is most
+    connected to (ties: lowest id). BFS partition ids are not spatially
+    ordered, so contiguous id blocks would make most ER rows halo rows."""
+    n_parts = e.n_parts
+    if world <= 1 or n_parts <= world:
+        return np.arange(n_parts, dtype=np.int64)
+    q = partition_quotient(e)
+    wsym = q + q.T
+    np.fill_diagonal(wsym, 0)
+    free = np.ones(n_parts, bool)
+    order = []
+    for g in range(world):
+        p0, p1 = part_range(n_parts, world, g)
+        size = p1 - p0
+        deg = np.where(free, (wsym * free[None, :]).sum(1), np.iinfo(np.int64).max)
+        seed = int(np.argmin(deg))
+        conn = np.zeros(n_parts, np.int64)
+        for _ in range(size):
+            free[seed] = False
+            order.append(seed)
+            conn += wsym[seed]
+            if not free.any():
+                break
+            cand = np.where(free, conn, -1)
+            seed = int(np.argmax(cand))
+    return np.asarray(order, np.int64)
+
+
+def renumber_partitions(e: EhybMatrix, order: np.ndarray) -> EhybMatrix:
+    """The same matrix with partitions renumbered (new partition i = old
+    partition order[i]): row r of old partition p becomes row
+    new(p)*vec + r%vec. Every row keeps its entries, k order and slicing, so
+    products are bitwise those of `e` under the block permutation; a derived
+    device-side layout for sharding, not a parity object."""
+    from .format import ReorderPlan
+
+    vec, warp = e.params.vec_cache_size, e.params.warp_size
+    n_parts = e.n_parts
+    order = np.asarray(order, np.int64)
+    if sorted(order.tolist()) != list(range(n_parts)):
+        raise ValueError("order must be a permutation of the partitions")
+    new_of_old = np.empty(n_parts, np.int64)
+    new_of_old[order] = np.arange(n_parts)
+
+    def rowmap(r):
+        r = np.asarray(r, np.int64)
+        return new_of_old[r // vec] * vec + r % vec
+
+    padded = e.padded_dimension
+    reorder = rowmap(e.plan.reorder_table)
+    inverse = np.empty_like(e.plan.inverse_table)
+    inverse[rowmap(np.arange(padded))] = e.plan.inverse_table
+    spp = vec // warp  # slices per partition
+    pos = np.asarray(e.position_ell, np.int64)
+    width = np.asarray(e.width_ell).reshape(n_parts, spp)[order].ravel()
+    seg_lo, seg_hi = pos[order * spp], pos[(order + 1) * spp]
+    take = np.concatenate([np.arange(a, b) for a, b in zip(seg_lo, seg_hi)]) if pos[-1] else         np.zeros(0, np.int64)
+    position = np.zeros(width.size + 1, np.int64)
+    np.cumsum(np.asarray(width, np.int64) * warp, out=position[1:])
+    position = position.astype(np.int32)
+    plan = ReorderPlan(reorder_table=reorder, inverse_table=inverse,
+                       arrange_table=e.plan.arrange_table, y_idx_er=rowmap(e.plan.y_idx_er),
+                       n_er_rows=e.plan.n_er_rows, dimension=e.dimension, padded_dimension=padded)
+    return EhybMatrix(
+        params=e.params, plan=plan, dimension=e.dimension, padded_dimension=padded,
+        val_ell=e.val_ell[take], col_ell=e.col_ell[take], position_ell=position,
+        width_ell=np.asarray(width, np.int32), part_boundary=e.part_boundary,
+        ell_row_widths=np.asarray(e.ell_row_widths).reshape(n_parts, vec)[order].ravel(),
+        val_er=e.val_er, col_er=rowmap(e.col_er).astype(np.uint32), position_er=e.position_er,
+        width_er=e.width_er, er_row_widths=e.er_row_widths)
+
+
 @dataclass
 class HaloPlan:
     rank: int
@@ -414,6 +506,8 @@ def bench_main(args, clock_cls=None):
         m = CooMatrix(n, n, r, c, v)
         nnz = m.nnz
         e = build_ehyb(m, tau=8, profile=b200_profile(world))
+        # contiguous rank blocks of a quotient-graph ordering of the partitions
+        e = renumber_partitions(e, group_partitions(e, world))
         write_ehyb_container(e, path)
         del m, r, c, v
     obj = [nnz]

@@ -170,3 +170,28 @@ def test_cg_converges_single_gpu(method):
     assert info["rel_residual"] < 1e-9
     assert np.max(np.abs(xs[real] - 1.0)) < 1e-7
     assert np.all(xs[~real] == 0.0)
+
+
+def test_partition_grouping_cuts_halo_and_keeps_results():
+    # renumbering partitions so each rank's contiguous block is compact in the
+    # quotient graph: same products (bitwise, C oracle), smaller halos
+    n, r, c, v = W.permute_symmetric(*W.stencil27(20, 20, 40), seed=1)
+    m = E.CooMatrix(n, n, r, c, v)
+    e = E.build_ehyb(m, tau=8, profile=E.DeviceProfile(24, 32, 8192))
+    x = W.deterministic_vector(n, 0)
+    y = E.unpermute_vector(c_oracle.spmv_ehyb(e, E.permute_vector(x, e.plan)), e.plan)
+    for world in (2, 4, 8):
+        order = D.group_partitions(e, world)
+        assert sorted(order.tolist()) == list(range(e.n_parts))
+        e2 = D.renumber_partitions(e, order)
+        e2.check()
+        y2 = E.unpermute_vector(c_oracle.spmv_ehyb(e2, E.permute_vector(x, e2.plan)), e2.plan)
+        assert y2.tobytes() == y.tobytes()
+
+        def total_halo(ee):
+            return sum(D.halo_columns(ee, *D.part_range(ee.n_parts, world, g)).size
+                       for g in range(world))
+
+        assert total_halo(e2) < total_halo(e)
+    with pytest.raises(ValueError, match="permutation"):
+        D.renumber_partitions(e, np.zeros(e.n_parts, np.int64))
