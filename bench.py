@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 METRIC = "SpMV GFLOP/s (2*nnz/t) and achieved HBM GB/s vs peak"
 UNIT = "GFLOP/s"
 FALLBACK_HBM_GBS = 6650.0
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e datasheet (SURVEY.md 8d secondary denominator)
 
 
 def log(*a):
@@ -461,6 +462,7 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
+                     "peak_spec": SPEC_HBM_GBS, "frac_spec": achieved / SPEC_HBM_GBS,
                      "algorithmic_bytes_per_launch": bmin,
                      "model": "nnz_ell*(tau+2) + nnz_er*(tau+4) + 2*n*tau (SURVEY.md 8d)"},
         "cpu_baseline": cpu,

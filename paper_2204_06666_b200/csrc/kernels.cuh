@@ -491,9 +491,6 @@ __device__ __forceinline__ T er_slice_compute(const SpmvParams<T>& P, const ErMe
 #ifndef EHYB_ER_PAIRS
 #define EHYB_ER_PAIRS 1
 #endif
-#ifndef EHYB_F32_PIPE
-#define EHYB_F32_PIPE 0
-#endif
 // Two ER slices at once (one warp, lane = row in each): their loads and x
 // gathers are issued together, so a latency-bound slice costs half the warp
 // time. b may be an empty claim (rw = -1, widths 0). Per row the order is the
@@ -1223,81 +1220,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       cs = cs_n;
     }
     publish();
-  } else if (EHYB_F32_PIPE && sizeof(T) == 4 && C32 && SMEM && P.do_ell && !P.ell_vec) {
-    // fp32: a continuous stream of 8-slot batches over the claimed chunks; the
-    // next batch's loads (same chunk, or the next chunk's first batch) are in
-    // flight while the current one is gathered and accumulated, so a warp
-    // keeps ~2 batches of HBM reads outstanding within the register budget
-    constexpr int U = 8;
-    struct Batch {
-      int64_t chunk;
-      int32_t eff, pos, k0;
-    };
-    auto width = [](int32_t eff) { return int(eff & kEffWidth); };
-    auto load = [&](const Batch& b, uint32_t* c, T* v) {
-      const int w = b.chunk < n_chunks ? width(b.eff) : 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        c[u] = 0;
-        v[u] = T(0);
-        if (b.k0 + u < w) {
-          const int64_t i = int64_t(b.pos) + lane + int64_t(b.k0 + u) * 32;
-          c[u] = __ldcs(P.col_ell + i);
-          v[u] = __ldcs(P.val_ell + i);
-        }
-      }
-    };
-    int64_t chunk = claim(&next_chunk);
-    EllMeta m = ell_meta(chunk);
-    int64_t nxt = claim(&next_chunk);
-    EllMeta mn = ell_meta(nxt);
-    Batch a{chunk, m.eff, m.pos, 0};
-    uint32_t ca[U], cb[U];
-    T va[U], vb[U];
-    load(a, ca, va);
-    T acc = T(0);
-    while (a.chunk < n_chunks) {
-      Batch b;
-      if (a.k0 + U < width(a.eff)) {
-        b = Batch{a.chunk, a.eff, a.pos, a.k0 + U};
-      } else {
-        b = Batch{nxt, mn.eff, mn.pos, 0};
-        nxt = claim(&next_chunk);
-        mn = ell_meta(nxt);
-      }
-      load(b, cb, vb);
-      if (win_pending) {
-        mbar_wait(&bar, phase);
-        win_pending = false;
-        if (P.timing && threadIdx.x == 0) P.timing[8 * cta + 1] = globaltimer();
-      }
-      const int w = width(a.eff);
-      T xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = win[ca[u]];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (a.k0 + u < w) acc = madd<STRICT>(acc, va[u], xv[u]);
-      if (a.k0 + U >= w) {  // last batch of the chunk
-        bool store = true;
-        if (a.eff & (kEffPadTail | kEffHasLong)) {
-          if (a.eff & kEffPadTail) acc = add_rn(acc, mul_rn(T(0), win[0]));
-          store = !((__ldg(P.long_bits + (row0 >> 5) + a.chunk) >> lane) & 1u);
-        }
-        publish();
-        if (store) P.y[row0 + a.chunk * 32 + lane] = acc;
-        unpublished = a.chunk;
-        acc = T(0);
-      }
-      a = b;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        ca[u] = cb[u];
-        va[u] = vb[u];
-      }
-    }
-    publish();
-    if (P.timing && lane == 0) atomicMax(P.timing + 8 * cta + 2, globaltimer());
   } else if (P.do_ell) {
     int64_t chunk = claim(&next_chunk);
     if (P.ell_ahead) {

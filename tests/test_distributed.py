@@ -195,3 +195,28 @@ def test_partition_grouping_cuts_halo_and_keeps_results():
         assert total_halo(e2) < total_halo(e)
     with pytest.raises(ValueError, match="permutation"):
         D.renumber_partitions(e, np.zeros(e.n_parts, np.int64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_grouped_shards_on_one_gpu_match_the_original(world):
+    # the multi-GPU bench path: renumber partitions by quotient-graph groups,
+    # shard the renumbered matrix, and get the original matrix's y
+    m, e = matrix(8)
+    e2 = D.renumber_partitions(e, D.group_partitions(e, world))
+    x = W.deterministic_vector(e.dimension, 0)
+    y_ref = E.spmv_ehyb_user(e, x)
+    xr2 = E.permute_vector(x, e2.plan)
+    y2 = np.empty(e2.padded_dimension)
+    for rank in range(world):
+        plan = D.plan_for(e2, rank, world)
+        A = D.DistributedEhyb(e2, device=0, plan=plan)
+        lo, hi = plan.p0 * plan.vec, plan.p1 * plan.vec
+        x_ext = A.new_ext()
+        x_ext[: plan.local_rows] = torch.from_numpy(xr2[lo:hi])
+        x_ext[plan.local_rows:] = torch.from_numpy(xr2[plan.halo_cols])
+        y = torch.empty(plan.local_rows, dtype=torch.float64, device="cuda:0")
+        A.spmv_local(x_ext, y)
+        torch.cuda.synchronize()
+        y2[lo:hi] = y.cpu().numpy()
+    assert E.unpermute_vector(y2, e2.plan).tobytes() == y_ref.tobytes()
