@@ -117,7 +117,10 @@ struct ehyb_dev {
   int32_t* pool_own_ptr = nullptr;
   int32_t* pool_own_idx = nullptr;
   void* pool_acc = nullptr;
-  unsigned int* cta_flag = nullptr;  // [max_ctas] persistent-mode publication
+  unsigned int* part_flag = nullptr;  // persistent mode: per-partition publication
+  int32_t* pool_grp = nullptr;         // pooled-slice range per iteration group
+  int32_t pool_groups = 0;
+  unsigned int* pool_gctr = nullptr;
   unsigned int* pool_ctr = nullptr;
   unsigned int* epoch_dev = nullptr;  // [2] launch epoch, CTAs finished (device-side: graph-safe)
   // own-ER shared-memory buffer
@@ -156,7 +159,7 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev, cta_flag,
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
@@ -214,7 +217,10 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_own_ptr = h->pool_own_ptr;
   P.pool_own_idx = h->pool_own_idx;
   P.pool_acc = static_cast<T*>(h->pool_acc);
-  P.cta_flag = h->cta_flag;
+  P.part_flag = h->part_flag;
+  P.pool_grp = h->pool_grp;
+  P.pool_groups = h->pool_groups;
+  P.pool_gctr = h->pool_gctr;
   P.epoch_dev = h->epoch_dev;
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
@@ -241,6 +247,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   if (P.er_sel == 2) {                 // the pool holds local rows only
     P.pool_lo = P.pool_hi;
     P.pool_own_ptr = nullptr;
+    P.part_flag = nullptr;  // no group drains (the group counters still reset)
   }
   void (*kern)(const SpmvParams<T>) = (do_ell && h->window_in_smem)
                                            ? spmv_fused_kernel<T, STRICT, C32, true, false>
@@ -557,6 +564,20 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     if (!any) break;
   }
   h->pool_hi = int64_t(order.size());
+  // several partitions per CTA: the pool is reordered (stable) into groups by
+  // the iteration in which the owner partition runs on its CTA (q / grid)
+  std::vector<int32_t> pool_gptr;
+  if (n_loc_parts > h->max_ctas && h->pool_hi > h->pool_lo &&
+      env_double("EHYB_POOL_DIRECT", 1.0) != 0.0) {
+    const int64_t grid = h->max_ctas;
+    const int64_t ng = (n_loc_parts + grid - 1) / grid;
+    std::stable_sort(order.begin() + h->pool_lo, order.end(),
+                     [&](const SliceRef& a, const SliceRef& b) { return a.q / grid < b.q / grid; });
+    pool_gptr.assign(static_cast<size_t>(ng) + 1, 0);
+    for (int64_t i = h->pool_lo; i < h->pool_hi; ++i) pool_gptr[size_t(order[size_t(i)].q / grid) + 1] += 1;
+    pool_gptr[0] = int32_t(h->pool_lo);
+    for (int64_t g = 0; g < ng; ++g) pool_gptr[size_t(g) + 1] += pool_gptr[size_t(g)];
+  }
   {
     int64_t max_own = 0;
     for (int64_t q = 0; q < n_loc_parts; ++q) max_own = std::max<int64_t>(max_own, int64_t(own[size_t(q)].size()));
@@ -826,10 +847,15 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(cudaMalloc(&h->pool_ctr, 16));
     CUDA_TRY(cudaMemset(h->pool_ctr, 0, 16));
     h->bytes += acc_bytes + size_t(n_loc_parts) * 8 + 32;
-    if (n_loc_parts > h->max_ctas && env_double("EHYB_POOL_DIRECT", 1.0) != 0.0) {
-      CUDA_TRY(cudaMalloc(&h->cta_flag, size_t(h->max_ctas) * 4 + 16));
-      CUDA_TRY(cudaMemset(h->cta_flag, 0, size_t(h->max_ctas) * 4 + 16));
-      h->bytes += size_t(h->max_ctas) * 4 + 16;
+    if (!pool_gptr.empty()) {
+      const int64_t ng = int64_t(pool_gptr.size()) - 1;
+      h->pool_groups = int32_t(ng);
+      CUDA_TRY(upload(&h->pool_grp, pool_gptr.data(), pool_gptr.size() * 4, &h->bytes));
+      CUDA_TRY(cudaMalloc(&h->pool_gctr, size_t(ng) * 8 + 16));
+      CUDA_TRY(cudaMemset(h->pool_gctr, 0, size_t(ng) * 8 + 16));
+      CUDA_TRY(cudaMalloc(&h->part_flag, size_t(n_loc_parts) * 4 + 16));
+      CUDA_TRY(cudaMemset(h->part_flag, 0, size_t(n_loc_parts) * 4 + 16));
+      h->bytes += size_t(ng) * 12 + size_t(n_loc_parts) * 4 + 48;
     }
   }
   *out = h.release();

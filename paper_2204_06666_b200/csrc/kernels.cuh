@@ -75,7 +75,14 @@ struct SpmvParams {
   const int32_t* __restrict__ pool_own_ptr;  // [n_parts+1] pooled slices of each partition
   const int32_t* __restrict__ pool_own_idx;  // their slice indices
   T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
-  unsigned int* cta_flag;           // [grid] epoch in which a CTA finished all its partitions
+  // several partitions per CTA: pooled slices grouped by the iteration in
+  // which their owner partition runs (p / grid); group g is drained by the
+  // ER-first warps during iteration g+1, rows finished in place once the
+  // owner partition is published (part_flag == epoch)
+  unsigned int* part_flag;          // [n_parts] epoch in which the partition's rows are final
+  const int32_t* __restrict__ pool_grp;  // [n_groups+1] pooled-slice range of each group
+  int32_t pool_groups;
+  unsigned int* pool_gctr;          // [2][n_groups] group claim counters by epoch
   unsigned int* epoch_dev;          // [2]: launch sequence number (>= 1), CTAs finished; kept
                                     // on the device so a captured CUDA graph replays correctly
   // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
@@ -772,31 +779,34 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
   return false;
 }
 
-// Pooled ER slices when CTAs run several partitions: drained after the
-// CTA's own partitions, two per claim, each row finished in place as
-// y[r] = y_ell[r] + sum once the CTA owning r has published all its
-// partitions (cta_flag == epoch). Publishing never waits on the pool, so the
-// waits always end.
+// Pooled ER slices of one iteration group when CTAs run several partitions:
+// claimed from the group's counter, two per claim (fp32), each row finished
+// in place as y[r] = y_final_of_owner[r] + sum once its owner partition is
+// published (part_flag == epoch). Group g's owners run in iteration g, and a
+// warp drains group g only after its own CTA has finished iteration g, so
+// every wait is on an earlier-or-equal iteration of another CTA: no cycle.
 template <typename T, bool STRICT>
-__device__ void pool_drain_direct(const SpmvParams<T>& P, int lane, uint32_t ep) {
-  if (P.pool_hi <= P.pool_lo) return;
-  unsigned int* ctr = P.pool_ctr + (ep & 1u);
+__device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, int g) {
+  if (g < 0 || g >= P.pool_groups) return;
+  const int64_t lo = __ldg(P.pool_grp + g), hi = __ldg(P.pool_grp + g + 1);
+  if (hi <= lo) return;
+  unsigned int* ctr = P.pool_gctr + (ep & 1u) * uint32_t(P.pool_groups) + uint32_t(g);
   auto finish = [&](const ErMeta& m, T acc) {
     if (m.rw < 0) return;
     const uint32_t r = uint32_t(m.rw & kRowMask);
-    const uint32_t owner = (r / uint32_t(P.vec)) % gridDim.x;
-    while (ld_acquire_gpu(P.cta_flag + owner) != ep) __nanosleep(64);
+    const uint32_t owner = r / uint32_t(P.vec);
+    while (ld_acquire_gpu(P.part_flag + owner) != ep) __nanosleep(64);
     P.y[r] = add_rn(__ldcg(P.y + r), acc);
   };
   constexpr unsigned kStep = (EHYB_ER_PAIRS && sizeof(T) == 4) ? 2u : 1u;
   for (;;) {
     unsigned int v = 0;
     if (lane == 0) v = atomicAdd(ctr, kStep);
-    const int64_t s = P.pool_lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
-    if (s >= P.pool_hi) break;
-    const ErMeta ma = er_claimed_meta(P, s, P.pool_hi, lane);
+    const int64_t s = lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
+    if (s >= hi) break;
+    const ErMeta ma = er_claimed_meta(P, s, hi, lane);
     if constexpr (kStep == 2u) {
-      const ErMeta mb = er_claimed_meta(P, s + 1, P.pool_hi, lane);
+      const ErMeta mb = er_claimed_meta(P, s + 1, hi, lane);
       T acc_a, acc_b;
       er_pair_compute<T, STRICT>(P, ma, mb, acc_a, acc_b);
       finish(ma, acc_a);
@@ -855,6 +865,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     if (P.timing) P.timing[8 * cta] = globaltimer();
     if (cta == 0 && P.pool_ctr) P.pool_ctr[(e0 + 1u) & 1u] = 0u;
     if (cta == 0 && P.lr_ctr) P.lr_ctr[(e0 + 1u) & 1u] = 0u;
+    if (cta == 0 && P.pool_gctr)
+      for (int g = 0; g < P.pool_groups; ++g)
+        P.pool_gctr[((e0 + 1u) & 1u) * uint32_t(P.pool_groups) + uint32_t(g)] = 0u;
     if constexpr (SMEM) {
       if (P.window_tma) {
         mbar_init(&bar, 1);
@@ -889,7 +902,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   const int64_t s1 = P.er_sel == 1 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part + 1);
   const uint32_t phase = uint32_t(it) & 1u;
 
-  if (it > 0) __syncthreads();  // every warp is done with the previous partition
+  if (it > 0) {
+    if (P.part_flag) __threadfence();  // the previous partition's y, gpu-wide
+    __syncthreads();                   // every warp is done with the previous partition
+    if (P.part_flag && threadIdx.x == 0) st_release_gpu(P.part_flag + (part - gridDim.x), ep);
+  }
   if (threadIdx.x == 0) {
     next_chunk = 0;
     next_er = 0;
@@ -1123,8 +1140,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       }
     }
     // pooled slices of every partition, hidden behind the other warps' ELL
-    // stream (a CTA running several partitions drains the pool after them)
+    // stream; with several partitions per CTA, the group whose owners ran in
+    // the previous iteration
     if (!persistent) pool_drain<T, STRICT>(P, lane, 0, ep);
+    else if (P.part_flag) pool_drain_group<T, STRICT>(P, lane, ep, it - 1);
   }
   const int64_t st_lo = RING ? int64_t(__ldg(P.part_stage_ptr + part)) : 0;
   const int64_t n_st = RING ? int64_t(__ldg(P.part_stage_ptr + part + 1)) - st_lo : 0;
@@ -1315,13 +1334,17 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   r_sbase += n_st;
   }  // partitions of this CTA
 
-  if (persistent && P.do_er && P.cta_flag) {
-    // several partitions per CTA: publish this CTA's rows, then drain the
-    // pool finishing rows in place (no scratch pass)
+  if (persistent && P.do_er && P.part_flag) {
+    // publish the last partition, then every group left (the last two at
+    // least) — rows finished in place as their owners are published
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) st_release_gpu(P.cta_flag + cta, ep);
-    pool_drain_direct<T, STRICT>(P, lane, ep);
+    if (threadIdx.x == 0) {
+      int last = cta;
+      while (last + int(gridDim.x) < P.n_parts) last += gridDim.x;
+      st_release_gpu(P.part_flag + last, ep);
+    }
+    for (int g = 0; g < P.pool_groups; ++g) pool_drain_group<T, STRICT>(P, lane, ep, g);
   } else if (persistent && P.do_er && P.pool_own_ptr) {
     pool_drain<T, STRICT>(P, lane, 0, ep);
     __syncthreads();

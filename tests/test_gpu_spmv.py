@@ -276,3 +276,49 @@ def test_persistent_ctas_multiple_partitions_per_cta():
     for _ in range(3):
         y, _ = E.spmv_ehyb(e, xr)
         assert y.tobytes() == want.tobytes()
+    # the split launches of the sharded path (local phase, then halo phase)
+    # with several partitions per CTA, two shards
+    from paper_2204_06666_b200 import distributed as D
+
+    for world in (1, 2):
+        for rank in range(world):
+            plan = D.plan_for(e, rank, world)
+            A = D.DistributedEhyb(e, device=0, plan=plan)
+            lo, hi = plan.p0 * plan.vec, plan.p1 * plan.vec
+            x_ext = A.new_ext()
+            x_ext[: plan.local_rows] = torch.from_numpy(xr[lo:hi])
+            x_ext[plan.local_rows:] = torch.from_numpy(xr[plan.halo_cols])
+            ys = torch.empty(plan.local_rows, dtype=torch.float64, device="cuda:0")
+            for _ in range(2):
+                A.spmv_local(x_ext, ys)
+                torch.cuda.synchronize()
+                assert ys.cpu().numpy().tobytes() == want[lo:hi].tobytes()
+
+
+def test_launch_kind_sequences_keep_per_launch_counters():
+    # any interleaving of full / local / halo launches must reset the
+    # per-launch counters of the next launch (they alternate by epoch parity)
+    import ctypes as C
+    from paper_2204_06666_b200 import _lib as L
+    from paper_2204_06666_b200 import distributed as D
+
+    for prof in (E.DeviceProfile(600, 32, 4096), E.DeviceProfile(24, 32, 8192)):
+        n, r, c, v = W.permute_symmetric(*W.stencil27(40, 40, 40), seed=4)
+        e = E.build_ehyb(E.CooMatrix(n, n, r, c, v), tau=8, profile=prof)
+        xr = E.permute_vector(W.deterministic_vector(n, 6), e.plan)
+        want = c_oracle.spmv_ehyb(e, xr)
+        plan = D.plan_for(e, 0, 1)
+        A = D.DistributedEhyb(e, device=0, plan=plan)
+        x_ext = A.new_ext()
+        x_ext[: plan.local_rows] = torch.from_numpy(xr)
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        seqs = [["ehyb_dev_spmv"], ["ehyb_dev_spmv_ell", "ehyb_dev_spmv_er"],
+                ["ehyb_dev_spmv_ell", "ehyb_dev_spmv_er"], ["ehyb_dev_spmv"],
+                ["ehyb_dev_spmv_ell", "ehyb_dev_spmv_er"], ["ehyb_dev_spmv"], ["ehyb_dev_spmv"]]
+        for seq in seqs:
+            y = torch.zeros(plan.local_rows, dtype=torch.float64, device="cuda:0")
+            for name in seq:
+                L.call(name, A._h, C.c_void_p(x_ext.data_ptr()), C.c_void_p(y.data_ptr()),
+                       L.MODE_STRICT, st)
+            torch.cuda.synchronize()
+            assert y.cpu().numpy().tobytes() == want.tobytes(), seq
