@@ -154,7 +154,7 @@ def renumber_partitions(e: EhybMatrix, order: np.ndarray) -> EhybMatrix:
         width_er=e.width_er, er_row_widths=e.er_row_widths)
 
 
-@dataclass
+@dataclass(eq=False)  # identity hash: plans key the device index-tensor cache
 class HaloPlan:
     rank: int
     world: int
@@ -246,8 +246,20 @@ def halo_exchange(x_ext, plan: HaloPlan, group=None, send_buf=None, async_op=Fal
     else:
         send_buf = x_ext[torch.from_numpy(plan.send_idx)]
     recv = x_ext[plan.local_rows: plan.local_rows + plan.n_halo]
+    if x_ext.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo has no CUDA all-to-all: stage through host memory (test path)
+        recv_h = torch.empty(recv.numel(), dtype=recv.dtype)
+        dist.all_to_all_single(recv_h, send_buf.cpu(), plan.recv_splits, plan.send_splits,
+                               group=group)
+        recv.copy_(recv_h)
+        return _Done() if async_op else None
     return dist.all_to_all_single(recv, send_buf, plan.recv_splits, plan.send_splits,
                                   group=group, async_op=async_op)
+
+
+class _Done:
+    def wait(self):
+        return True
 
 
 _idx_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
@@ -483,7 +495,10 @@ def bench_main(args, clock_cls=None):
         os.environ.setdefault(k, v)  # allow a single-process run without torchrun
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    # EHYB_DIST_BACKEND=gloo: a functional check of the multi-rank flow with
+    # several ranks sharing one GPU (NCCL needs one GPU per rank)
+    backend = os.environ.get("EHYB_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", str(rank))) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     # the driver parses one JSON line from stdout: keep NCCL's banner off it
     if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
@@ -492,7 +507,10 @@ def bench_main(args, clock_cls=None):
     saved = os.dup(1)
     os.dup2(2, 1)
     try:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
     finally:
         sys.stdout.flush()
@@ -519,6 +537,7 @@ def bench_main(args, clock_cls=None):
     t_prep = time.perf_counter() - t0
     A = DistributedEhyb(e, device=local)
     bmin_total = engine.min_bytes(e)
+    e_full = e if rank == 0 else None  # the single-GPU product checks the sharded one
     from . import workloads as W
 
     xg = W.deterministic_vector(e.dimension, 0)
@@ -598,6 +617,21 @@ def bench_main(args, clock_cls=None):
                           "allreduces_per_iter": 1 if method == "chronopoulos-gear" else 2}
     if clocks is not None:
         clocks.__exit__(None, None, None)
+    # parity: the gathered sharded y against one single-GPU launch (rank 0)
+    A.spmv(x_ext, y)
+    torch.cuda.synchronize()
+    parts = [None] * world if rank == 0 else None
+    dist.gather_object(y.cpu().numpy(), parts, dst=0)
+    parity = None
+    if rank == 0:
+        from .device import DeviceMatrix
+
+        dm = DeviceMatrix(e_full, local)
+        y_one = dm.spmv(torch.from_numpy(xr).to(f"cuda:{local}", dm.torch_dtype)).cpu().numpy()
+        ok = np.concatenate(parts).tobytes() == y_one.tobytes()
+        parity = "bitwise == single-GPU product" if ok else "MISMATCH"
+        del dm
+    e_full = None
     if rank == 0:
         flops = 2 * nnz
         out = {
@@ -622,9 +656,10 @@ def bench_main(args, clock_cls=None):
                            "slice, synchronised (max over ranks)"},
             "clocks": clocks.summary() if clocks is not None else None,
             "halo_values_rank0": A.plan.n_halo,
+            "parity": parity, "backend": backend,
             "cg": cg_res,
             "preprocessing_s": t_prep,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (1 if world == 1 else 3) * args.steps,
         }
         print(json.dumps(out), flush=True)
     dist.barrier()

@@ -106,6 +106,10 @@ def test_plans_are_consistent():
                 rseg = np.cumsum([0] + pg.recv_splits)
                 assert np.array_equal(sent, pg.halo_cols[rseg[q]:rseg[q + 1]])
         assert sum(p.local_rows for p in plans) == e.padded_dimension
+        # plans key the device index cache (identity hash), one tensor per plan
+        t = D._idx_tensor(plans[0], torch.device("cpu"))
+        assert D._idx_tensor(plans[0], torch.device("cpu")) is t
+        assert np.array_equal(t.numpy(), plans[0].send_idx)
 
 
 def heavy_matrix(tau=8):
