@@ -224,6 +224,47 @@ __device__ __forceinline__ void prefetch_slice(const T* val, const uint16_t* col
 // lane keeps 2U independent loads in flight (U = 8 for fp64, 16 for fp32:
 // the same bytes in flight per lane); the tail batch is predicated. The
 // accumulation order is k ascending (reference order).
+// ELL stream loads. EHYB_LD_HINT selects the PTX form (measured in
+// DESIGN.md §8): 0 = ld.global.cs (evict-first), 1/2 = ld.global.cs with an
+// L2 prefetch size of 128/256 B, 3 = ld.global.nc.L1::no_allocate.L2::256B
+#ifndef EHYB_LD_HINT
+#define EHYB_LD_HINT 0
+#endif
+#if EHYB_LD_HINT == 1
+#define EHYB_LD_Q "ld.global.cs.L2::128B"
+#elif EHYB_LD_HINT == 2
+#define EHYB_LD_Q "ld.global.cs.L2::256B"
+#elif EHYB_LD_HINT == 3
+#define EHYB_LD_Q "ld.global.nc.L1::no_allocate.L2::256B"
+#endif
+__device__ __forceinline__ uint32_t ld_stream(const uint16_t* p) {
+#if EHYB_LD_HINT == 0
+  return __ldcs(p);
+#else
+  unsigned short v;
+  asm volatile(EHYB_LD_Q ".u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return v;
+#endif
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if EHYB_LD_HINT == 0
+  return __ldcs(p);
+#else
+  double v;
+  asm volatile(EHYB_LD_Q ".f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#endif
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+#if EHYB_LD_HINT == 0
+  return __ldcs(p);
+#else
+  float v;
+  asm volatile(EHYB_LD_Q ".f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#endif
+}
+
 #ifndef EHYB_UNROLL_F32
 #define EHYB_UNROLL_F32 8
 #endif
@@ -246,9 +287,9 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
     uint32_t c[U];
     T v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
+    for (int u = 0; u < U; ++u) c[u] = ld_stream(col + pos + int64_t(k + u) * 32);
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
+    for (int u = 0; u < U; ++u) v[u] = ld_stream(val + pos + int64_t(k + u) * 32);
     // a warp's first chunk issues its stream loads before the window has
     // landed: the TMA copy and the first HBM round trip overlap
     if constexpr (WAIT) {
@@ -268,8 +309,8 @@ __device__ __forceinline__ T ell_slice32(const T* __restrict__ val,
       c[u] = 0;
       v[u] = T(0);
       if (k + u < w) {
-        c[u] = __ldcs(col + pos + int64_t(k + u) * 32);
-        v[u] = __ldcs(val + pos + int64_t(k + u) * 32);
+        c[u] = ld_stream(col + pos + int64_t(k + u) * 32);
+        v[u] = ld_stream(val + pos + int64_t(k + u) * 32);
       }
     }
     if constexpr (WAIT) {
