@@ -515,7 +515,15 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // own / pool split: partition q keeps the prefix of its ER slices that fits
   // its share of the mean per-CTA cost (ELL slots + er_cost * ER entries);
   // the rest joins a pool any CTA may claim once its own work is done
-  const double pool_factor = env_double("EHYB_POOL_FACTOR", 0.95);
+  // small partitions (at most two ELL chunks per warp, e.g. cfg1): the pool's
+  // extra round trips cost more than the balance it buys; more ER-first
+  // warps and no claim-ahead (profiles/sweep_r2_small_cfg1.txt)
+  const bool small = chunks <= 2 * int64_t(h->threads / 32);
+  if (small) {
+    h->er_warps = 16;
+    h->ell_ahead = h->er_ahead = 0;
+  }
+  const double pool_factor = env_double("EHYB_POOL_FACTOR", small ? 1e30 : 0.95);
   const double er_cost = env_double("EHYB_ER_COST", 5.0);
   std::vector<double> ell_cost(static_cast<size_t>(n_loc_parts)), er_total(static_cast<size_t>(n_loc_parts), 0.0);
   double total = 0.0;
