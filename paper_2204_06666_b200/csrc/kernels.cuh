@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   __shared__ int ell_finished;
   __shared__ uint32_t chunk_done[kMaxChunks / 32];
   __shared__ uint32_t er_done[kMaxErBuf / 32];
-  __shared__ T lr_stage[64];  // long-row products (warp 0)
+  __shared__ __align__(16) T lr_stage[64];  // long-row products (warp 0)
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int cta = blockIdx.x;
