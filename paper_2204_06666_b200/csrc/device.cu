@@ -117,6 +117,7 @@ struct ehyb_dev {
   int32_t* pool_own_ptr = nullptr;
   int32_t* pool_own_idx = nullptr;
   void* pool_acc = nullptr;
+  void* own_acc = nullptr;  // own ER sums beyond the shared-memory buffer
   unsigned int* part_flag = nullptr;  // persistent mode: per-partition publication
   int32_t* pool_grp = nullptr;         // pooled-slice range per iteration group
   int32_t pool_groups = 0;
@@ -159,7 +160,7 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, own_acc, pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
@@ -217,6 +218,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_own_ptr = h->pool_own_ptr;
   P.pool_own_idx = h->pool_own_idx;
   P.pool_acc = static_cast<T*>(h->pool_acc);
+  P.own_acc = static_cast<T*>(h->own_acc);
   P.part_flag = h->part_flag;
   P.pool_grp = h->pool_grp;
   P.pool_groups = h->pool_groups;
@@ -576,6 +578,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // several partitions per CTA: the pool is reordered (stable) into groups by
   // the iteration in which the owner partition runs on its CTA (q / grid)
   std::vector<int32_t> pool_gptr;
+  bool own_scratch = false;
   if (n_loc_parts > h->max_ctas && h->pool_hi > h->pool_lo &&
       env_double("EHYB_POOL_DIRECT", 1.0) != 0.0) {
     const int64_t grid = h->max_ctas;
@@ -591,6 +594,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     int64_t max_own = 0;
     for (int64_t q = 0; q < n_loc_parts; ++q) max_own = std::max<int64_t>(max_own, int64_t(own[size_t(q)].size()));
     h->er_buf_slices = int(std::min<int64_t>(h->er_buf_slices, max_own));
+    // partitions with more own ER slices than the shared-memory buffer holds
+    // (large windows, e.g. cfg5) spill the rest to a global scratch, so the
+    // ER-first warps still finish them during the ELL phase
+    own_scratch = max_own > h->er_buf_slices && env_double("EHYB_OWN_SCRATCH", 0.0) != 0.0;
     h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
     // ELL ring (C == 32, TMA-staged window): shared memory left after the
     // window, at least 2 chunks of the widest slice; the own-ER buffer gives
@@ -727,6 +734,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   }
   h->er_slices = n_sl;
   h->er_slots = eslots;
+  if (own_scratch) {
+    CUDA_TRY(cudaMalloc(&h->own_acc, size_t(std::max<int64_t>(n_sl, 1)) * 32 * tb));
+    h->bytes += size_t(std::max<int64_t>(n_sl, 1)) * 32 * tb;
+  }
   CUDA_TRY(upload(&h->er_part_ptr, part_ptr.data(), part_ptr.size() * 4, &h->bytes));
   CUDA_TRY(upload(&h->er_part_mid, part_mid.data(), part_mid.size() * 4, &h->bytes));
   CUDA_TRY(upload(&h->er_pos, epos.data(), epos.size() * 8, &h->bytes));

@@ -75,6 +75,7 @@ struct SpmvParams {
   const int32_t* __restrict__ pool_own_ptr;  // [n_parts+1] pooled slices of each partition
   const int32_t* __restrict__ pool_own_idx;  // their slice indices
   T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
+  T* own_acc;                       // [er_slices*32] own ER row sums beyond the smem buffer (or null)
   // several partitions per CTA: pooled slices grouped by the iteration in
   // which their owner partition runs (p / grid); group g is drained by the
   // ER-first warps during iteration g+1, rows finished in place once the
@@ -1005,12 +1006,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   // longest dependent work of the launch
   if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) long_rows_warp<T, STRICT>(P, lane, lr_stage, ep);
 
-  // own ER slices [s0, s1): the first n_buf are computed into a shared-memory
-  // buffer at any time (ER-first warps overlap them with the ELL stream) and
-  // combined with y_ell at the end; the rest finish directly against y_ell
+  // own ER slices [s0, s1): the first n_buf are computed into a buffer at
+  // any time (ER-first warps overlap them with the ELL stream) and combined
+  // with y_ell at the end; the rest finish directly against y_ell
   const int64_t n_own = s1 - s0;
-  const int64_t n_buf = (P.do_er && P.do_ell) ? (n_own < P.er_buf_slices ? n_own : P.er_buf_slices) : 0;
+  // own slices beyond the shared-memory buffer go to a global scratch
+  // (own_acc) when the handle has one, up to the done-bitmap capacity
+  const int64_t buf_cap = P.own_acc ? int64_t(kMaxErBuf) : int64_t(P.er_buf_slices);
+  const int64_t n_buf = (P.do_er && P.do_ell) ? (n_own < buf_cap ? n_own : buf_cap) : 0;
   T* er_buf = reinterpret_cast<T*>(smem_raw + P.er_buf_offset);
+  auto buf_at = [&](int64_t idx) -> T* {
+    return idx < P.er_buf_slices ? er_buf + idx * 32 + lane
+                                 : P.own_acc + (s0 + idx) * 32 + lane;
+  };
 
   auto wait_chunk = [&](int64_t r) {
     const int64_t ch = (r - row0) >> 5;
@@ -1135,7 +1143,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   };
   auto own_post = [&](int64_t idx, const ErMeta& m, T acc, T yv, bool have_y) {
     if (idx < n_buf) {
-      er_buf[idx * 32 + lane] = acc;
+      *buf_at(idx) = acc;
       __threadfence_block();
       __syncwarp();
       if (lane == 0) atomicOr(&er_done[idx >> 5], 1u << (idx & 31));
@@ -1155,7 +1163,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     const bool have_y = own_pre(idx, m, yv);
     const T acc = er_slice_compute<T, STRICT>(P, m);
     if (idx < n_buf) {
-      er_buf[idx * 32 + lane] = acc;
+      *buf_at(idx) = acc;
       __threadfence_block();
       __syncwarp();
       if (lane == 0) atomicOr(&er_done[idx >> 5], 1u << (idx & 31));
@@ -1346,7 +1354,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       if (rw >= 0) {
         const int64_t r = rw & kRowMask;
         wait_chunk(r);
-        P.y[r] = add_rn(__ldcg(P.y + r), er_buf[idx * 32 + lane]);
+        P.y[r] = add_rn(__ldcg(P.y + r), idx < P.er_buf_slices ? er_buf[idx * 32 + lane]
+                                                                : __ldcg(buf_at(idx)));
       }
     }
     stamp(5);
