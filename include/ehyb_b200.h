@@ -24,6 +24,10 @@
  *  - Device entry points take CUDA device pointers and a cudaStream_t passed
  *    as void*; launches are stream-ordered and never synchronise the host
  *    unless stated.
+ *  - A handle keeps per-launch counters on the device (alternating by a
+ *    device-side launch epoch, so captured CUDA graphs replay correctly):
+ *    launches of one handle must be ordered (one stream, or events between
+ *    streams); different handles are independent.
  */
 #ifndef EHYB_B200_H
 #define EHYB_B200_H
