@@ -267,6 +267,25 @@ EHYB_API int ehyb_dev_spmv_ell(ehyb_dev* h, const void* x_ext, void* y_local, in
 EHYB_API int ehyb_dev_spmv_er(ehyb_dev* h, const void* x_ext, void* y_local, int mode,
                               void* stream);
 
+/* P2P halo exchange (one launch per SpMV, no NCCL): the shard handle owns
+ * x_ext ([owned | halo], tau bytes each) and a 64-byte flag block, both
+ * IPC-shareable. Every rank publishes IPC handles of both (ehyb_ipc_handle),
+ * maps its peers' (ehyb_ipc_open) and passes them with its pull plan (per
+ * halo slot: source rank and offset in that rank's x_ext) to
+ * ehyb_dev_p2p_setup; served_per_spmv = values the peers pull from this rank
+ * per SpMV. ehyb_dev_spmv_p2p then runs ELL, local ER, the halo pull from
+ * peer memory and the halo rows in one launch; it returns (stream-ordered)
+ * only after the peers have pulled from this rank, so the next kernel may
+ * overwrite x_ext. All ranks must issue the same sequence of p2p SpMVs. */
+EHYB_API int ehyb_dev_p2p_alloc(ehyb_dev* h, void** x_ext, void** flags);
+EHYB_API int ehyb_ipc_handle(const void* dev_ptr, void* out_handle /* 64 bytes */);
+EHYB_API int ehyb_ipc_open(const void* handle, int device, void** out_ptr);
+EHYB_API int ehyb_ipc_close(void* ptr);
+EHYB_API int ehyb_dev_p2p_setup(ehyb_dev* h, int32_t world, int32_t rank, void* const* peer_x,
+                                void* const* peer_flags, const int32_t* pull_src,
+                                const int64_t* pull_off, int64_t served_per_spmv);
+EHYB_API int ehyb_dev_spmv_p2p(ehyb_dev* h, void* y_local, int mode, void* stream);
+
 /* Gather x_local[idx[i]] into a packed send buffer (halo pack). */
 EHYB_API int ehyb_dev_gather(const void* src, const int64_t* idx_dev, int64_t count, void* dst,
                              int32_t tau, void* stream);

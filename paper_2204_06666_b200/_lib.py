@@ -109,6 +109,13 @@ _PROTOS = {
     "ehyb_dev_spmv_host": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
     "ehyb_dev_spmv_host_many": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                           C.c_int64, C.c_int, C.c_int, vp]),
+    "ehyb_dev_p2p_alloc": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "ehyb_ipc_handle": (C.c_int, [vp, vp]),
+    "ehyb_ipc_open": (C.c_int, [vp, C.c_int, C.POINTER(C.c_void_p)]),
+    "ehyb_ipc_close": (C.c_int, [vp]),
+    "ehyb_dev_p2p_setup": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
+                                     C.POINTER(C.c_void_p), vp, vp, C.c_int64]),
+    "ehyb_dev_spmv_p2p": (C.c_int, [vp, vp, C.c_int, vp]),
     "ehyb_dev_gather": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int32, vp]),
     "ehyb_dev_dot": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp, vp]),
     "ehyb_dev_cg_xr": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int32, vp, vp]),

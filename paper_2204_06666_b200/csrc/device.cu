@@ -118,6 +118,16 @@ struct ehyb_dev {
   int32_t* pool_own_idx = nullptr;
   void* pool_acc = nullptr;
   void* own_acc = nullptr;  // own ER sums beyond the shared-memory buffer
+  // P2P halo exchange (shards): x_ext and flags owned by the handle (IPC-able),
+  // the pull plan and the peers' mapped buffers
+  void* p2p_x = nullptr;
+  unsigned long long* p2p_flags = nullptr;
+  int32_t* pull_src = nullptr;
+  int64_t* pull_off = nullptr;
+  void** peer_x_dev = nullptr;
+  unsigned long long** peer_flags_dev = nullptr;
+  unsigned long long p2p_seq = 0, served_per_spmv = 0;
+  bool p2p_ready = false, p2p_active = false;
   unsigned int* part_flag = nullptr;  // persistent mode: per-partition publication
   int32_t* pool_grp = nullptr;         // pooled-slice range per iteration group
   int32_t pool_groups = 0;
@@ -160,7 +170,8 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, own_acc, pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, own_acc, p2p_x, p2p_flags, pull_src, pull_off, peer_x_dev, peer_flags_dev,
+                    pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
@@ -219,6 +230,15 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_own_idx = h->pool_own_idx;
   P.pool_acc = static_cast<T*>(h->pool_acc);
   P.own_acc = static_cast<T*>(h->own_acc);
+  P.n_halo = h->n_halo;
+  P.local_rows = h->local_rows;
+  P.pull_src = h->pull_src;
+  P.pull_off = h->pull_off;
+  P.peer_x = reinterpret_cast<T* const*>(h->peer_x_dev);
+  P.peer_flags = h->peer_flags_dev;
+  P.my_flags = h->p2p_flags;
+  P.seq = h->p2p_seq;
+  P.served_per_spmv = h->served_per_spmv;
   P.part_flag = h->part_flag;
   P.pool_grp = h->pool_grp;
   P.pool_groups = h->pool_groups;
@@ -275,6 +295,9 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
       P.ch_stage = h->ch_stage;
       smem = h->ring_offset + h->ring_bytes;
     }
+  }
+  if constexpr (C32) {
+    if (h->p2p_active) kern = spmv_fused_kernel<T, STRICT, true, true, false, true>;
   }
   if (!(do_ell && do_er)) {
     P.er_buf_slices = 0;
@@ -1136,6 +1159,107 @@ EHYB_API int ehyb_dev_spmv_host_many(ehyb_dev* h, const void* const* x_hosts,
     }
     CUDA_TRY(cudaStreamSynchronize(h->s_out));
     CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+// ------------------------------------------------ P2P halo exchange
+EHYB_API int ehyb_dev_p2p_alloc(ehyb_dev* h, void** x_ext, void** flags) {
+  EHYB_TRY {
+    if (!h || !h->shard) return fail("p2p buffers need a shard handle");
+    DeviceGuard guard(h->device);
+    if (!h->p2p_x) {
+      const size_t xb = size_t(h->local_rows + h->n_halo) * size_t(h->tau);
+      CUDA_TRY(cudaMalloc(&h->p2p_x, std::max<size_t>(xb, 16)));
+      CUDA_TRY(cudaMemset(h->p2p_x, 0, std::max<size_t>(xb, 16)));
+      CUDA_TRY(cudaMalloc(&h->p2p_flags, 64));
+      CUDA_TRY(cudaMemset(h->p2p_flags, 0, 64));
+      h->bytes += xb + 64;
+    }
+    if (x_ext) *x_ext = h->p2p_x;
+    if (flags) *flags = h->p2p_flags;
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_ipc_handle(const void* dev_ptr, void* out_handle) {
+  EHYB_TRY {
+    if (!dev_ptr || !out_handle) return fail("null argument");
+    cudaIpcMemHandle_t hd;
+    CUDA_TRY(cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr)));
+    std::memcpy(out_handle, &hd, sizeof(hd));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_ipc_open(const void* handle, int device, void** out_ptr) {
+  EHYB_TRY {
+    if (!handle || !out_ptr) return fail("null argument");
+    DeviceGuard guard(device);
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    CUDA_TRY(cudaIpcOpenMemHandle(out_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_ipc_close(void* ptr) {
+  EHYB_TRY {
+    if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_p2p_setup(ehyb_dev* h, int32_t world, int32_t rank, void* const* peer_x,
+                                void* const* peer_flags, const int32_t* pull_src,
+                                const int64_t* pull_off, int64_t served_per_spmv) {
+  EHYB_TRY {
+    if (!h || !h->p2p_x) return fail("call ehyb_dev_p2p_alloc first");
+    if (h->warp != 32 || !h->window_in_smem || !h->window_tma || h->ring_bytes)
+      return fail("p2p exchange needs 32-row slices and a TMA-staged window");
+    if (world < 1 || rank < 0 || rank >= world) return fail("bad world / rank");
+    DeviceGuard guard(h->device);
+    std::vector<void*> px(static_cast<size_t>(world)), pf(static_cast<size_t>(world));
+    for (int q = 0; q < world; ++q) {
+      px[size_t(q)] = q == rank ? h->p2p_x : peer_x[q];
+      pf[size_t(q)] = q == rank ? static_cast<void*>(h->p2p_flags) : peer_flags[q];
+    }
+    if (h->peer_x_dev) cudaFree(h->peer_x_dev);
+    if (h->peer_flags_dev) cudaFree(h->peer_flags_dev);
+    if (h->pull_src) cudaFree(h->pull_src);
+    if (h->pull_off) cudaFree(h->pull_off);
+    h->peer_x_dev = nullptr;
+    h->peer_flags_dev = nullptr;
+    h->pull_src = nullptr;
+    h->pull_off = nullptr;
+    size_t dummy = 0;
+    CUDA_TRY(upload(&h->peer_x_dev, px.data(), px.size() * sizeof(void*), &dummy));
+    CUDA_TRY(upload(&h->peer_flags_dev, pf.data(), pf.size() * sizeof(void*), &dummy));
+    CUDA_TRY(upload(&h->pull_src, pull_src, size_t(h->n_halo) * 4, &dummy));
+    CUDA_TRY(upload(&h->pull_off, pull_off, size_t(h->n_halo) * 8, &dummy));
+    h->served_per_spmv = (unsigned long long)served_per_spmv;
+    h->p2p_ready = true;
+    return 0;
+  }
+  EHYB_CATCH
+}
+
+EHYB_API int ehyb_dev_spmv_p2p(ehyb_dev* h, void* y_local, int mode, void* stream) {
+  EHYB_TRY {
+    if (!h || !h->p2p_ready) return fail("p2p exchange not set up (ehyb_dev_p2p_setup)");
+    if (!y_local) return fail("null argument");
+    DeviceGuard guard(h->device);
+    h->p2p_seq += 1;
+    h->p2p_active = true;
+    const cudaError_t e = launch_spmv(h, h->p2p_x, y_local, mode, true, true,
+                                      static_cast<cudaStream_t>(stream));
+    h->p2p_active = false;
+    CUDA_TRY(e);
     return 0;
   }
   EHYB_CATCH

@@ -76,6 +76,18 @@ struct SpmvParams {
   const int32_t* __restrict__ pool_own_idx;  // their slice indices
   T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
   T* own_acc;                       // [er_slices*32] own ER row sums beyond the smem buffer (or null)
+  // P2P halo (shards, exchange = peer memory): the launch itself pulls the
+  // halo from the peers' x buffers over NVLink and finishes halo rows once
+  // its pulls are complete — one launch per SpMV, no NCCL
+  int64_t n_halo;                   // halo slots, x_ext[local_rows + i]
+  int64_t local_rows;
+  const int32_t* __restrict__ pull_src;   // [n_halo] peer rank of each halo slot
+  const int64_t* __restrict__ pull_off;   // [n_halo] offset in that peer's x
+  T* const* peer_x;                       // [world] peers' x buffers (own entry unused)
+  unsigned long long* const* peer_flags;  // [world] peers' flag blocks
+  unsigned long long* my_flags;           // {ready seq, served (cum.), pulled (cum.)}
+  unsigned long long seq;                 // SpMV sequence number (>= 1)
+  unsigned long long served_per_spmv;     // values peers pull from this rank per SpMV
   // several partitions per CTA: pooled slices grouped by the iteration in
   // which their owner partition runs (p / grid); group g is drained by the
   // ER-first warps during iteration g+1, rows finished in place once the
@@ -859,6 +871,47 @@ __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, 
   }
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// P2P halo pull of one warp: halo slots [lo, hi) (grouped by source peer)
+// read from the peers' x once each peer has published this SpMV's x; then
+// the pulled values are counted for the peers (served: they may overwrite x)
+// and for this rank (pulled: halo rows may start).
+template <typename T>
+__device__ void p2p_pull(const SpmvParams<T>& P, int lane, int64_t lo, int64_t hi) {
+  T* x_ext = const_cast<T*>(P.x);
+  int64_t i = lo;
+  while (i < hi) {
+    const int src = __ldg(P.pull_src + i);
+    int64_t j = i;  // end of this peer's run
+    while (j < hi && __ldg(P.pull_src + j) == src) ++j;
+    if (lane == 0)
+      while (ld_acquire_sys_u64(P.peer_flags[src]) < P.seq) __nanosleep(100);
+    __syncwarp();
+    const T* px = P.peer_x[src];
+    for (int64_t k = i + lane; k < j; k += 32) x_ext[P.local_rows + k] = px[__ldg(P.pull_off + k)];
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) atomicAdd_system(P.peer_flags[src] + 1, (unsigned long long)(j - i));
+    i = j;
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0 && hi > lo) atomicAdd(P.my_flags + 2, (unsigned long long)(hi - lo));
+}
+
 __device__ __forceinline__ int lds_volatile(const uint32_t* p, uint32_t bit) {
   return (*reinterpret_cast<const volatile uint32_t*>(p) & bit) != 0;
 }
@@ -873,7 +926,7 @@ constexpr int kMaxErBuf = 2048;                        // buffered own ER slices
 // warp moves straight on to the partition's ER slices (no CTA barrier). An
 // ER row whose ELL chunk is still in flight waits on that chunk's done bit,
 // so y[r] = y_ell[r] + er_acc keeps the reference's order of operations.
-template <typename T, bool STRICT, bool C32, bool SMEM, bool RING>
+template <typename T, bool STRICT, bool C32, bool SMEM, bool RING, bool P2P = false>
 __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvParams<T> P) {
   static_assert(!RING || (C32 && SMEM), "the ELL ring needs 32-row slices and a staged window");
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1002,9 +1055,34 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   }
   const T* win = SMEM ? xs : xwin;
   if (P.timing && threadIdx.x == 0 && !win_pending) P.timing[8 * cta + 1] = globaltimer();
+  if constexpr (P2P) {
+   if (it == 0) {
+    if (cta == 0 && threadIdx.x == 0) {  // this rank's x is final: peers may pull
+      __threadfence_system();
+      st_release_sys_u64(P.my_flags, P.seq);
+    }
+    const int nw = int(blockDim.x >> 5);
+    if (wid >= nw - 2) {  // two pull warps per CTA, the halo split over the grid
+      const int64_t per = (P.n_halo + int64_t(gridDim.x) * 2 - 1) / (int64_t(gridDim.x) * 2);
+      const int64_t lo = (int64_t(cta) * 2 + (wid - (nw - 2))) * per;
+      const int64_t hi = lo + per < P.n_halo ? lo + per : P.n_halo;
+      if (lo < hi) p2p_pull(P, lane, lo, hi);
+    }
+   }
+  }
+  auto wait_halo = [&]() {  // every halo value of this SpMV is in x_ext
+    if constexpr (!P2P) return;
+    if (lane == 0)
+      while (ld_acquire_gpu_u64(P.my_flags + 2) < P.seq * (unsigned long long)P.n_halo)
+        __nanosleep(64);
+    __syncwarp();
+  };
   // long rows first (warp 0 of every CTA): their serial chains are the
   // longest dependent work of the launch
-  if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) long_rows_warp<T, STRICT>(P, lane, lr_stage, ep);
+  if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) {
+    wait_halo();
+    long_rows_warp<T, STRICT>(P, lane, lr_stage, ep);
+  }
 
   // own ER slices [s0, s1): the first n_buf are computed into a buffer at
   // any time (ER-first warps overlap them with the ELL stream) and combined
@@ -1013,7 +1091,17 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   // own slices beyond the shared-memory buffer go to a global scratch
   // (own_acc) when the handle has one, up to the done-bitmap capacity
   const int64_t buf_cap = P.own_acc ? int64_t(kMaxErBuf) : int64_t(P.er_buf_slices);
-  const int64_t n_buf = (P.do_er && P.do_ell) ? (n_own < buf_cap ? n_own : buf_cap) : 0;
+  // P2P: slices [n_loc, n_own) read halo values (wait for the pulls)
+  const int64_t n_loc = P2P ? int64_t(__ldg(P.er_part_mid + part)) - s0 : n_own;
+  const int64_t n_bufable = P2P ? n_loc : n_own;
+  const int64_t n_buf = (P.do_er && P.do_ell) ? (n_bufable < buf_cap ? n_bufable : buf_cap) : 0;
+  bool halo_seen = !P2P;
+  auto need_halo = [&](int64_t idx) {
+    if (!halo_seen && idx >= n_loc) {
+      wait_halo();
+      halo_seen = true;
+    }
+  };
   T* er_buf = reinterpret_cast<T*>(smem_raw + P.er_buf_offset);
   auto buf_at = [&](int64_t idx) -> T* {
     return idx < P.er_buf_slices ? er_buf + idx * 32 + lane
@@ -1124,6 +1212,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   // a row whose ELL value is already final has y read before the slice's
   // loads, so that round trip overlaps them
   auto own_pre = [&](int64_t idx, const ErMeta& m, T& yv) -> bool {
+    need_halo(idx);
     const bool direct = idx >= n_buf && m.rw >= 0;
     bool have_y = false;
     if (direct) {
@@ -1157,6 +1246,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     }
   };
   auto finish_own_er = [&](int64_t idx, const ErMeta& m) {
+    need_halo(idx);
     const bool direct = idx >= n_buf && m.rw >= 0;
     const int64_t r = m.rw & kRowMask;
     T yv = T(0);
@@ -1424,6 +1514,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   }
 
   __syncthreads();
+  if (P2P && cta == 0 && threadIdx.x == 0) {
+    // this rank's x may be overwritten by the next stream operation only
+    // once every peer has pulled its halo values from it
+    while (ld_acquire_sys_u64(P.my_flags + 1) < P.seq * P.served_per_spmv) __nanosleep(100);
+  }
   if (threadIdx.x == 0) {
     if (P.timing) P.timing[8 * cta + 3] = globaltimer();
     // the last CTA to finish advances the launch epoch

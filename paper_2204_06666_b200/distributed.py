@@ -279,12 +279,21 @@ class DistributedEhyb:
     """This rank's shard of a globally assembled EhybMatrix on its GPU."""
 
     def __init__(self, e: EhybMatrix, group=None, device: int | None = None,
-                 plan: HaloPlan | None = None):
+                 plan: HaloPlan | None = None, exchange: str = "nccl"):
+        """exchange "nccl": pack + NCCL all-to-all overlapped with the local
+        launch, then the halo launch. exchange "p2p": the halo is pulled from
+        the peers' x buffers over peer memory (CUDA IPC / NVLink) inside ONE
+        fused launch per SpMV — no NCCL, no pack kernel, no second launch;
+        x lives in a handle-owned, peer-mapped buffer (`ext_buffer()`)."""
         import torch
 
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange = exchange
         self.group = group
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.plan = build_halo_plan(e, group) if plan is None else plan
+        self.plan_n_parts = e.n_parts
         self.tau = e.params.tau
         self.dtype = torch.float32 if self.tau == 4 else torch.float64
         self.nnz_local = int(e.ell_row_widths[self.plan.p0 * self.plan.vec:
@@ -305,11 +314,79 @@ class DistributedEhyb:
         self.n_ext = self.plan.local_rows + self.plan.n_halo
         self._send = torch.empty(max(1, int(sum(self.plan.send_splits))), dtype=self.dtype,
                                  device=f"cuda:{self.device}")
+        self._x_p2p = None
+        if exchange == "p2p":
+            self._setup_p2p()
+
+    def _setup_p2p(self):
+        """IPC handles of the handle-owned x_ext and flag block go to every
+        rank; each rank maps its peers' and hands the pull plan (source rank
+        and offset of every halo slot) to the device handle."""
+        import torch
+        import torch.distributed as dist
+
+        xp, fp = C.c_void_p(), C.c_void_p()
+        L.call("ehyb_dev_p2p_alloc", self._h, C.byref(xp), C.byref(fp))
+
+        class _Buf:  # zero-copy torch view of the handle-owned x_ext
+            def __init__(self, ptr, n, typestr):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                                 "data": (ptr, False), "version": 3,
+                                                 "strides": None}
+
+        self._x_p2p = torch.as_tensor(
+            _Buf(xp.value, self.n_ext, "<f4" if self.tau == 4 else "<f8"),
+            device=f"cuda:{self.device}")
+
+        def handle(ptr):
+            buf = (C.c_char * 64)()
+            L.call("ehyb_ipc_handle", C.c_void_p(ptr), buf)
+            return bytes(buf)
+
+        mine = (handle(xp.value), handle(fp.value))
+        world, rank = self.plan.world, self.plan.rank
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=self.group)
+        self._peer_ptrs = []
+        px = (C.c_void_p * world)()
+        pf = (C.c_void_p * world)()
+        for q in range(world):
+            if q == rank:
+                continue
+            for arr, hb in ((px, allh[q][0]), (pf, allh[q][1])):
+                ptr = C.c_void_p()
+                L.call("ehyb_ipc_open", C.create_string_buffer(hb, 64), self.device,
+                       C.byref(ptr))
+                arr[q] = ptr.value
+                self._peer_ptrs.append(ptr.value)
+        vec = self.plan.vec
+        ranges = [part_range(self.plan_n_parts, world, q) for q in range(world)]
+        starts = np.array([r0 * vec for r0, _ in ranges], np.int64)
+        halo = np.asarray(self.plan.halo_cols, np.int64)
+        src = (np.searchsorted(starts, halo, side="right") - 1).astype(np.int32)
+        off = (halo - starts[src]).astype(np.int64)
+        L.call("ehyb_dev_p2p_setup", self._h, world, rank, px, pf, C.c_void_p(src.ctypes.data),
+               C.c_void_p(off.ctypes.data), int(sum(self.plan.send_splits)))
+        self._p2p_keep = (src, off)
+        lib = L.lib()
+        self._p2p_finalizer = weakref.finalize(
+            self, lambda ptrs: [lib.ehyb_ipc_close(C.c_void_p(p)) for p in ptrs],
+            list(self._peer_ptrs))
 
     def new_ext(self):
+        """A fresh zeroed x in the [owned | halo] layout the SpMV reads."""
         import torch
 
         return torch.zeros(self.n_ext, dtype=self.dtype, device=f"cuda:{self.device}")
+
+    def ext_buffer(self):
+        """The x_ext the SpMV reads without a copy. p2p: the handle-owned,
+        peer-mapped buffer (one per handle: write the owned part, the halo
+        part is pulled by the kernel; spmv on any other x_ext first copies its
+        owned part here). NCCL: a fresh buffer like new_ext()."""
+        if self._x_p2p is not None:
+            return self._x_p2p
+        return self.new_ext()
 
     def spmv_local(self, x_ext, y_local, *, fma: bool = False):
         """Both phases on an x_ext whose halo is already filled (no exchange)."""
@@ -329,6 +406,12 @@ class DistributedEhyb:
 
         mode = L.MODE_FMA if fma else L.MODE_STRICT
         st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        if self._x_p2p is not None:
+            # one fused launch: ELL, local ER, halo pull from peer memory, halo rows
+            if x_ext.data_ptr() != self._x_p2p.data_ptr():
+                self._x_p2p[: self.local_rows].copy_(x_ext[: self.local_rows])
+            L.call("ehyb_dev_spmv_p2p", self._h, C.c_void_p(y_local.data_ptr()), mode, st)
+            return y_local
         xp, yp = C.c_void_p(x_ext.data_ptr()), C.c_void_p(y_local.data_ptr())
         if self.plan.world == 1:
             L.call("ehyb_dev_spmv", self._h, xp, yp, mode, st)
@@ -352,7 +435,7 @@ class DistributedEhyb:
         import torch
 
         if not hasattr(self, "_x_ext"):
-            self._x_ext = self.new_ext()
+            self._x_ext = self.ext_buffer()
             self._y_loc = torch.empty(self.local_rows, dtype=self.dtype,
                                       device=f"cuda:{self.device}")
         self._x_ext[: self.local_rows].copy_(torch.as_tensor(x_local), non_blocking=True)
@@ -392,7 +475,7 @@ def cg(A: DistributedEhyb, b_local, maxiter: int = 100, tol: float = 0.0,
     tau = A.tau
     x = torch.zeros(n, dtype=A.dtype, device=dev)
     r = b_local.clone()
-    p = A.new_ext()
+    p = A.ext_buffer()
     p[:n].copy_(r)
     q = torch.empty(n, dtype=A.dtype, device=dev)
     sc = torch.zeros(4, dtype=torch.float64, device=dev)  # rr, pq, rr_new, |b|^2
@@ -435,7 +518,7 @@ def _cg_cg(A: DistributedEhyb, b_local, maxiter: int, tol: float):
     st = C.c_void_p(torch.cuda.current_stream(A.device).cuda_stream)
     tau = A.tau
     x = torch.zeros(n, dtype=A.dtype, device=dev)
-    r = A.new_ext()  # r lives in the [owned | halo] layout the SpMV reads
+    r = A.ext_buffer()  # r lives in the [owned | halo] layout the SpMV reads
     r[:n].copy_(b_local)
     p = torch.zeros(n, dtype=A.dtype, device=dev)
     s = torch.zeros(n, dtype=A.dtype, device=dev)
@@ -535,7 +618,25 @@ def bench_main(args, clock_cls=None):
     if rank != 0:
         e = read_ehyb_container(path)
     t_prep = time.perf_counter() - t0
-    A = DistributedEhyb(e, device=local)
+    # exchange: the fused peer-memory pull (one launch per SpMV) by default at
+    # N > 1, NCCL if any rank cannot map its peers (decided collectively)
+    exchange = os.environ.get("EHYB_EXCHANGE", "p2p" if world > 1 else "nccl")
+    A = None
+    if exchange == "p2p":
+        ok = torch.ones(1, dtype=torch.int64,
+                        device=f"cuda:{local}" if backend == "nccl" else "cpu")
+        try:
+            A = DistributedEhyb(e, device=local, exchange="p2p")
+        except Exception as ex:  # noqa: BLE001 - reported, then the NCCL path
+            print(f"p2p exchange unavailable on rank {rank}: {ex}", file=sys.stderr)
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok) == 0:
+            A, exchange = None, "nccl"
+    if A is None:
+        A = DistributedEhyb(e, device=local)
+    # the other exchange, timed beside it (N > 1)
+    A_nccl = DistributedEhyb(e, device=local) if (exchange == "p2p" and world > 1) else None
     bmin_total = engine.min_bytes(e)
     e_full = e if rank == 0 else None  # the single-GPU product checks the sharded one
     from . import workloads as W
@@ -545,7 +646,7 @@ def bench_main(args, clock_cls=None):
 
     xr = permute_vector(xg, e.plan)
     lo, hi = A.plan.p0 * A.plan.vec, A.plan.p1 * A.plan.vec
-    x_ext = A.new_ext()
+    x_ext = A.ext_buffer()
     x_ext[: A.local_rows].copy_(torch.from_numpy(xr[lo:hi]))
     y = torch.empty(A.local_rows, dtype=A.dtype, device=x_ext.device)
     del e
@@ -571,6 +672,25 @@ def bench_main(args, clock_cls=None):
                      device=x_ext.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t)
+    t_nccl = None
+    if A_nccl is not None:
+        xn = A_nccl.new_ext()
+        xn[: A_nccl.local_rows].copy_(torch.from_numpy(xr[lo:hi]))
+        yn = torch.empty_like(y)
+        for _ in range(args.warmup):
+            A_nccl.spmv(xn, yn)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            A_nccl.spmv(xn, yn)
+        ev1.record()
+        ev1.synchronize()
+        tn = torch.tensor([ev0.elapsed_time(ev1) / 1e3 / args.steps], dtype=torch.float64,
+                          device=x_ext.device)
+        dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+        t_nccl = float(tn)
+        del A_nccl, xn, yn
     # end to end: per step the owned x slice H2D (pinned), exchange + product,
     # owned y slice D2H, synchronised; max over ranks
     x_pin = torch.from_numpy(np.ascontiguousarray(xr[lo:hi])).pin_memory()
@@ -617,7 +737,9 @@ def bench_main(args, clock_cls=None):
                           "allreduces_per_iter": 1 if method == "chronopoulos-gear" else 2}
     if clocks is not None:
         clocks.__exit__(None, None, None)
-    # parity: the gathered sharded y against one single-GPU launch (rank 0)
+    # parity: the gathered sharded y against one single-GPU launch (rank 0);
+    # x_ext is rewritten (p2p: CG used the same handle-owned buffer)
+    x_ext[: A.local_rows].copy_(torch.from_numpy(xr[lo:hi]))
     A.spmv(x_ext, y)
     torch.cuda.synchronize()
     parts = [None] * world if rank == 0 else None
@@ -628,8 +750,14 @@ def bench_main(args, clock_cls=None):
 
         dm = DeviceMatrix(e_full, local)
         y_one = dm.spmv(torch.from_numpy(xr).to(f"cuda:{local}", dm.torch_dtype)).cpu().numpy()
-        ok = np.concatenate(parts).tobytes() == y_one.tobytes()
+        y_all = np.concatenate(parts)
+        ok = y_all.tobytes() == y_one.tobytes()
         parity = "bitwise == single-GPU product" if ok else "MISMATCH"
+        if not ok:
+            bad = np.flatnonzero(y_all.view(np.int64) != y_one.view(np.int64))
+            print(f"parity: {bad.size} rows differ, first {bad[:8].tolist()}, "
+                  f"values {[(float(y_all[i]), float(y_one[i])) for i in bad[:4]]}",
+                  file=sys.stderr)
         del dm
     e_full = None
     if rank == 0:
@@ -642,8 +770,11 @@ def bench_main(args, clock_cls=None):
             "data": "synthetic",
             "config": {"workload": f"27-point stencil {128 * world}x128x128, random symmetric "
                                    f"permutation, P=148x{world} (N=1: cfg2; N=8: cfg5 rows)",
-                       "nnz": nnz, "parallelism": f"row shards x{world}, NCCL halo all-to-all "
-                                                  "overlapped with the ELL phase",
+                       "nnz": nnz, "parallelism": (
+                           f"row shards x{world}, halo pulled from peer memory inside one "
+                           f"fused launch" if exchange == "p2p" else
+                           f"row shards x{world}, NCCL halo all-to-all overlapped with the "
+                           f"local launch"),
                        "l2_policy": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": bmin_total / t_step / 1e9 / world,
                          "peak": 6457.4, "unit": "GB/s (per GPU)",
@@ -656,10 +787,14 @@ def bench_main(args, clock_cls=None):
                            "slice, synchronised (max over ranks)"},
             "clocks": clocks.summary() if clocks is not None else None,
             "halo_values_rank0": A.plan.n_halo,
-            "parity": parity, "backend": backend,
+            "parity": parity, "backend": backend, "exchange": exchange,
+            "nccl_exchange": None if t_nccl is None else {
+                "ms_per_step": t_nccl * 1e3, "value": flops / t_nccl / 1e9,
+                "how": "pack kernel + NCCL all_to_all overlapped with the local launch, "
+                       "then the halo launch"},
             "cg": cg_res,
             "preprocessing_s": t_prep,
-            "gpu_launches": (1 if world == 1 else 3) * args.steps,
+            "gpu_launches": (1 if (world == 1 or exchange == "p2p") else 3) * args.steps,
         }
         print(json.dumps(out), flush=True)
     dist.barrier()
