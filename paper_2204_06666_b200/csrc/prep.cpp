@@ -1,3 +1,4 @@
+#include <memory>
 // EHYB host preprocessing — bit-exact C++17 restatement of the reference
 // pipeline (arXiv 2204.06666 reference package `ehyb`):
 //   compute_params      format.py:83-107   (Eq.1-2)
@@ -96,38 +97,58 @@ struct MT19937 {
   }
 };
 
-// Fenwick tree over positions of the degree order: 1 = still unassigned.
-struct Fenwick {
-  std::vector<int32_t> t;
-  int64_t n = 0, top = 1;
+// Rank/select set over positions of the degree order: 1 = still unassigned.
+// A bitset with per-512-bit block counts and per-64-block super counts: an
+// assignment clears one bit and decrements two counters (one random cache
+// line instead of a Fenwick tree's ~log2(n) scattered nodes); the rare seed
+// queries scan counters.
+struct RankSet {
+  static constexpr int kBlk = 9, kSup = 15;  // 512 bits per block, 32768 per super block
+  std::vector<uint64_t> bits;
+  std::vector<int32_t> blk, sup;
+  int64_t n = 0;
   void init_ones(int64_t n_) {
     n = n_;
-    t.assign(size_t(n) + 1, 0);
-    for (int64_t i = 1; i <= n; ++i) {
-      t[size_t(i)] += 1;
-      int64_t j = i + (i & -i);
-      if (j <= n) t[size_t(j)] += t[size_t(i)];
+    bits.assign(size_t((n + 63) >> 6), ~0ull);
+    if (n & 63) bits.back() = (1ull << (n & 63)) - 1;
+    blk.assign(size_t((n >> kBlk) + 1), 0);
+    sup.assign(size_t((n >> kSup) + 1), 0);
+    for (int64_t i = 0; i < n; i += 64) {
+      const int c = __builtin_popcountll(bits[size_t(i >> 6)]);
+      blk[size_t(i >> kBlk)] += c;
+      sup[size_t(i >> kSup)] += c;
     }
-    while (top * 2 <= n) top *= 2;
   }
-  void dec(int64_t pos) {  // 0-based
-    for (int64_t i = pos + 1; i <= n; i += i & -i) t[size_t(i)] -= 1;
+  void dec(int64_t pos) {  // 0-based, the bit must be set
+    bits[size_t(pos >> 6)] &= ~(1ull << (pos & 63));
+    blk[size_t(pos >> kBlk)] -= 1;
+    sup[size_t(pos >> kSup)] -= 1;
   }
-  int64_t prefix(int64_t cnt) const {  // sum over [0, cnt)
+  int64_t prefix(int64_t cnt) const {  // set bits in [0, cnt)
     int64_t s = 0;
-    for (int64_t i = cnt; i > 0; i -= i & -i) s += t[size_t(i)];
+    const int64_t S = cnt >> kSup;
+    for (int64_t i = 0; i < S; ++i) s += sup[size_t(i)];
+    for (int64_t i = S << (kSup - kBlk); i < (cnt >> kBlk); ++i) s += blk[size_t(i)];
+    for (int64_t w = (cnt >> kBlk) << (kBlk - 6); w < (cnt >> 6); ++w)
+      s += __builtin_popcountll(bits[size_t(w)]);
+    if (cnt & 63) s += __builtin_popcountll(bits[size_t(cnt >> 6)] & ((1ull << (cnt & 63)) - 1));
     return s;
   }
   // smallest 0-based position p with prefix(p + 1) >= target (target >= 1)
   int64_t find(int64_t target) const {
-    int64_t pos = 0;
-    for (int64_t step = top; step; step >>= 1) {
-      if (pos + step <= n && t[size_t(pos + step)] < target) {
-        pos += step;
-        target -= t[size_t(pos)];
-      }
+    int64_t i = 0;
+    while (sup[size_t(i)] < target) target -= sup[size_t(i++)];
+    int64_t b = i << (kSup - kBlk);
+    while (blk[size_t(b)] < target) target -= blk[size_t(b++)];
+    int64_t w = b << (kBlk - 6);
+    for (;; ++w) {
+      const int c = __builtin_popcountll(bits[size_t(w)]);
+      if (c >= target) break;
+      target -= c;
     }
-    return pos;
+    uint64_t x = bits[size_t(w)];
+    for (int64_t k = 1; k < target; ++k) x &= x - 1;  // drop the lowest target-1 set bits
+    return (w << 6) + __builtin_ctzll(x);
   }
 };
 
@@ -169,48 +190,131 @@ EHYB_API int ehyb_build_graph(int64_t n, int64_t nnz, const int64_t* rows, const
                               int64_t* adj_ptr, int32_t** out_adj, int64_t* out_n_adj) {
   EHYB_TRY {
     if (n < 0 || n > INT32_MAX) return ehyb::fail("graph dimension outside int32 range");
-    // raw symmetric lists: every off-diagonal (u,v) contributes v to u and u to v
-    std::vector<std::atomic<int64_t>> cnt(size_t(n) + 1);
-#pragma omp parallel for schedule(static) if (n > kParallelMin)
-    for (int64_t i = 0; i <= n; ++i) cnt[size_t(i)].store(0, std::memory_order_relaxed);
-#pragma omp parallel for schedule(static) if (nnz > kParallelMin)
-    for (int64_t e = 0; e < nnz; ++e) {
-      int64_t u = rows[e], v = cols[e];
-      if (u != v) {
-        cnt[size_t(u)].fetch_add(1, std::memory_order_relaxed);
-        cnt[size_t(v)].fetch_add(1, std::memory_order_relaxed);
+    // Every off-diagonal (u,v) contributes the keys u<<32|v and v<<32|u; the
+    // sorted distinct keys are np.unique over src*n+dst. Cache-friendly
+    // two-level radix order: keys are scattered into buckets of 2^shift
+    // consecutive vertices by per-thread histograms (no atomics), then each
+    // bucket (L2-sized) is counting-sorted by vertex and every neighbour list
+    // sorted and deduplicated locally.
+    int shift = 0;
+    while ((n >> shift) > 4096) ++shift;
+    const int64_t n_b = (n >> shift) + 1;
+    // fixed work split (independent of how many threads OpenMP grants)
+    const int64_t nt = nnz > kParallelMin ? std::max(1, omp_get_max_threads()) : 1;
+    const int64_t chunk = cdiv(std::max<int64_t>(nnz, 1), nt);
+    std::vector<int64_t> hist(size_t(nt) * size_t(n_b), 0);
+#pragma omp parallel for schedule(static, 1) if (nt > 1)
+    for (int64_t t = 0; t < nt; ++t) {
+      int64_t* h = hist.data() + size_t(t) * size_t(n_b);
+      const int64_t e0 = std::min(nnz, t * chunk), e1 = std::min(nnz, e0 + chunk);
+      // row-grouped inputs repeat a bucket many times in a row: count runs in
+      // a register instead of a load-increment-store chain on one counter
+      int64_t run_b = 0, run_c = 0;
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t u = rows[e], v = cols[e];
+        if (u == v) continue;
+        const int64_t bu = u >> shift;
+        if (bu != run_b) {
+          h[run_b] += run_c;
+          run_b = bu;
+          run_c = 0;
+        }
+        ++run_c;
+        h[v >> shift]++;
+      }
+      h[run_b] += run_c;
+    }
+    std::vector<int64_t> bstart(size_t(n_b) + 1, 0);
+    {
+      int64_t acc = 0;
+      for (int64_t i = 0; i < n_b; ++i) {
+        bstart[size_t(i)] = acc;
+        for (int64_t t = 0; t < nt; ++t) {
+          int64_t& h = hist[size_t(t) * size_t(n_b) + size_t(i)];
+          const int64_t c = h;
+          h = acc;  // chunk t's write cursor in bucket i
+          acc += c;
+        }
+      }
+      bstart[size_t(n_b)] = acc;
+    }
+    const int64_t n_keys = bstart[size_t(n_b)];
+    // uninitialised (no serial zero-fill): first touched by the parallel scatter
+    std::unique_ptr<uint64_t[]> keys(new uint64_t[size_t(std::max<int64_t>(n_keys, 1))]);
+#pragma omp parallel for schedule(static, 1) if (nt > 1)
+    for (int64_t t = 0; t < nt; ++t) {
+      int64_t* h = hist.data() + size_t(t) * size_t(n_b);
+      const int64_t e0 = std::min(nnz, t * chunk), e1 = std::min(nnz, e0 + chunk);
+      for (int64_t e = e0; e < e1; ++e) {
+        const uint64_t u = uint64_t(rows[e]), v = uint64_t(cols[e]);
+        if (u != v) {
+          keys[size_t(h[u >> shift]++)] = (u << 32) | v;
+          keys[size_t(h[v >> shift]++)] = (v << 32) | u;
+        }
       }
     }
-    std::vector<int64_t> raw_ptr(size_t(n) + 1, 0);
-    for (int64_t i = 0; i < n; ++i) raw_ptr[size_t(i) + 1] = raw_ptr[size_t(i)] + cnt[size_t(i)].load();
-    std::vector<int32_t> raw(size_t(raw_ptr[size_t(n)]));
-#pragma omp parallel for schedule(static) if (n > kParallelMin)
-    for (int64_t i = 0; i < n; ++i) cnt[size_t(i)].store(raw_ptr[size_t(i)], std::memory_order_relaxed);
-#pragma omp parallel for schedule(static) if (nnz > kParallelMin)
-    for (int64_t e = 0; e < nnz; ++e) {
-      int64_t u = rows[e], v = cols[e];
-      if (u != v) {
-        raw[size_t(cnt[size_t(u)].fetch_add(1, std::memory_order_relaxed))] = int32_t(v);
-        raw[size_t(cnt[size_t(v)].fetch_add(1, std::memory_order_relaxed))] = int32_t(u);
-      }
-    }
-    // per-vertex sort + unique == np.unique over src*n+dst keys
+    const bool serial = nt == 1;
+    // per bucket (L2-sized): LSD radix sort of the keys by neighbour id, then
+    // a stable counting pass by vertex, then deduplication — each neighbour
+    // list ends up ascending and distinct, compacted at the bucket's start
+    std::unique_ptr<int32_t[]> vals(new int32_t[size_t(std::max<int64_t>(n_keys, 1))]);
     std::vector<int64_t> uniq(size_t(n), 0);
-#pragma omp parallel for schedule(dynamic, 4096) if (n > kParallelMin)
-    for (int64_t i = 0; i < n; ++i) {
-      int32_t* b = raw.data() + raw_ptr[size_t(i)];
-      int32_t* e = raw.data() + raw_ptr[size_t(i) + 1];
-      std::sort(b, e);
-      uniq[size_t(i)] = std::unique(b, e) - b;
+    int vbits = 0;
+    while (vbits < 32 && (int64_t(1) << vbits) < n) ++vbits;
+    constexpr int kRB = 11;
+#pragma omp parallel if (!serial)
+    {
+      std::vector<uint64_t> bufa, bufb;
+      std::vector<int64_t> cnt(size_t(1) << kRB);
+#pragma omp for schedule(dynamic, 1)
+      for (int64_t bi = 0; bi < n_b; ++bi) {
+        const int64_t v0 = bi << shift, v1 = std::min<int64_t>(n, (bi + 1) << shift);
+        if (v0 >= v1) continue;
+        const int64_t k0 = bstart[size_t(bi)], k1 = bstart[size_t(bi) + 1], nk = k1 - k0;
+        bufa.assign(keys.get() + k0, keys.get() + k1);
+        bufb.resize(size_t(nk));
+        auto pass = [&](int lo, int bits, uint64_t base) {  // stable counting pass on key bits [lo, lo+bits)
+          const uint64_t mask = (uint64_t(1) << bits) - 1;
+          std::fill(cnt.begin(), cnt.begin() + (int64_t(1) << bits), 0);
+          for (int64_t k = 0; k < nk; ++k) cnt[size_t(((bufa[size_t(k)] - base) >> lo) & mask)]++;
+          int64_t acc = 0;
+          for (int64_t i = 0; i < (int64_t(1) << bits); ++i) {
+            const int64_t c = cnt[size_t(i)];
+            cnt[size_t(i)] = acc;
+            acc += c;
+          }
+          for (int64_t k = 0; k < nk; ++k) {
+            const uint64_t key = bufa[size_t(k)];
+            bufb[size_t(cnt[size_t(((key - base) >> lo) & mask)]++)] = key;
+          }
+          bufa.swap(bufb);
+        };
+        for (int lo = 0; lo < vbits; lo += kRB) pass(lo, std::min(kRB, vbits - lo), 0);
+        if (shift > 0) pass(32, shift, uint64_t(v0) << 32);  // by vertex within the bucket
+        int32_t* out = vals.get() + k0;
+        int64_t w = 0;
+        uint64_t prev = ~uint64_t(0);
+        for (int64_t k = 0; k < nk; ++k) {
+          const uint64_t key = bufa[size_t(k)];
+          if (key == prev) continue;
+          prev = key;
+          out[w++] = int32_t(uint32_t(key));
+          uniq[size_t(key >> 32)]++;
+        }
+      }
     }
     adj_ptr[0] = 0;
     for (int64_t i = 0; i < n; ++i) adj_ptr[i + 1] = adj_ptr[i] + uniq[size_t(i)];
-    int64_t total = adj_ptr[n];
+    const int64_t total = adj_ptr[n];
     int32_t* adj = static_cast<int32_t*>(std::malloc(size_t(std::max<int64_t>(total, 1)) * 4));
     if (!adj) return ehyb::fail_oom();
-#pragma omp parallel for schedule(static) if (n > kParallelMin)
-    for (int64_t i = 0; i < n; ++i)
-      std::memcpy(adj + adj_ptr[i], raw.data() + raw_ptr[size_t(i)], size_t(uniq[size_t(i)]) * 4);
+#pragma omp parallel for schedule(dynamic, 16) if (!serial)
+    for (int64_t bi = 0; bi < n_b; ++bi) {
+      const int64_t v0 = bi << shift, v1 = std::min<int64_t>(n, (bi + 1) << shift);
+      if (v0 >= v1) continue;
+      std::memcpy(adj + adj_ptr[v0], vals.get() + bstart[size_t(bi)],
+                  size_t(adj_ptr[v1] - adj_ptr[v0]) * 4);
+    }
     *out_adj = adj;
     *out_n_adj = total;
     return 0;
@@ -228,7 +332,9 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
                         std::to_string(capacity) + " cannot hold " + std::to_string(n) +
                         " vertices");
     MT19937 rng(seed);
-    for (int64_t v = 0; v < n; ++v) assignment[v] = -1;
+    // part ids in a compact int32 copy (half the cache footprint of the
+    // caller's int64 array), written back at the end
+    std::vector<int32_t> part(size_t(n), -1);
     for (int64_t p = 0; p < n_parts; ++p) sizes[p] = 0;
 
     // stable degree order of connected vertices (counting sort = stable argsort)
@@ -254,19 +360,19 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
         }
       }
     }
-    Fenwick fw;
+    RankSet fw;
     fw.init_ones(n_conn);
     int64_t cursor = 0;
 
     auto assign = [&](int64_t v, int64_t pid) {
-      assignment[v] = pid;
+      part[v] = int32_t(pid);
       sizes[pid] += 1;
       if (pos_of[size_t(v)] >= 0) fw.dec(pos_of[size_t(v)]);
     };
     // partition.py:131-144: first unassigned vertex of minimum degree; when the
     // unassigned part of its equal-degree run holds >1 vertex, draw its index
     auto next_seed = [&]() -> int64_t {
-      while (cursor < n_conn && assignment[by_degree[size_t(cursor)]] >= 0) ++cursor;
+      while (cursor < n_conn && part[by_degree[size_t(cursor)]] >= 0) ++cursor;
       if (cursor >= n_conn) return -1;
       int64_t d = adj_ptr[by_degree[size_t(cursor)] + 1] - adj_ptr[by_degree[size_t(cursor)]];
       int64_t run_end = deg_start[size_t(d) + 1];
@@ -287,11 +393,23 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
       size_t qh = 0, qt = 0;
       queue[qt++] = int32_t(start);
       while (qh < qt && sizes[pid] < capacity) {
+        // software pipeline over the queue (the permuted graphs have no
+        // locality): adjacency offsets 16 ahead, lists 8 ahead, the
+        // neighbours' assignment words 4 ahead
+        if (qh + 16 < qt) __builtin_prefetch(adj_ptr + queue[qh + 16]);
+        if (qh + 8 < qt) __builtin_prefetch(adj + adj_ptr[queue[qh + 8]]);
+        if (qh + 4 < qt) {
+          const int64_t f = queue[qh + 4];
+          for (int64_t j = adj_ptr[f]; j < adj_ptr[f + 1]; ++j) {
+            __builtin_prefetch(part.data() + adj[j], 1);
+            __builtin_prefetch(pos_of.data() + adj[j]);
+          }
+        }
         int64_t u = queue[qh++];
         bool full = false;
         for (int64_t j = adj_ptr[u]; j < adj_ptr[u + 1]; ++j) {
           int64_t w = adj[j];
-          if (assignment[w] < 0) {
+          if (part[w] < 0) {
             assign(w, pid);
             ++grown;
             queue[qt++] = int32_t(w);
@@ -316,7 +434,7 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
       for (int64_t v = 0; v < n; ++v) {
         if (adj_ptr[v + 1] != adj_ptr[v]) continue;
         while (sizes[pid] >= capacity) pid = (pid + 1) % n_parts;
-        assignment[v] = pid;
+        part[v] = pid;
         sizes[pid] += 1;
         pid = (pid + 1) % n_parts;
       }
@@ -329,11 +447,13 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
     std::vector<int64_t> cnt(size_t(n_parts), 0);
     std::vector<int64_t> touched;
     for (int64_t v = 0; v < n; ++v) {
+      if (v + 8 < n)  // neighbours' assignments of a vertex 8 ahead (random lines)
+        for (int64_t j = adj_ptr[v + 8]; j < adj_ptr[v + 9]; ++j) __builtin_prefetch(part.data() + adj[j]);
       if (adj_ptr[v + 1] == adj_ptr[v]) continue;
-      int64_t a = assignment[v];
+      int64_t a = part[v];
       touched.clear();
       for (int64_t j = adj_ptr[v]; j < adj_ptr[v + 1]; ++j) {
-        int64_t q = assignment[adj[j]];
+        int64_t q = part[adj[j]];
         if (cnt[size_t(q)]++ == 0) touched.push_back(q);
       }
       int64_t internal = cnt[size_t(a)];
@@ -349,13 +469,15 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
       for (int64_t q : touched) cnt[size_t(q)] = 0;
       if (best >= 0 && best_sc > internal) {
         bool a_was_full = sizes[a] >= capacity;
-        assignment[v] = best;
+        part[v] = int32_t(best);
         sizes[a] -= 1;
         sizes[best] += 1;
         if (a_was_full && sizes[a] < capacity) ++nonfull;
         if (sizes[best] >= capacity) --nonfull;
       }
     }
+#pragma omp parallel for schedule(static) if (n > kParallelMin)
+    for (int64_t v = 0; v < n; ++v) assignment[v] = part[size_t(v)];
     return 0;
   }
   EHYB_CATCH
