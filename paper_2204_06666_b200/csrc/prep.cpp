@@ -157,6 +157,101 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // below this trip count a loop runs serially (OpenMP fork/join would dominate)
 constexpr int64_t kParallelMin = 1 << 15;
 
+// Entries grouped by row and ordered by (column, entry index) — the order of
+// np.lexsort((cols, rows)) including duplicate coordinates — as a row pointer
+// plus the sorted columns and values. Per-chunk histograms scatter the
+// entries into buckets of 2^shift consecutive rows (chunks in entry order, so
+// the scatter is stable), then each L2-sized bucket is LSD-radix sorted by
+// column and by row (stable passes: duplicates keep entry order).
+void group_rows(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                const double* values, std::vector<int64_t>& rptr,
+                std::unique_ptr<int32_t[]>& scol, std::unique_ptr<double[]>& sval) {
+  int shift = 0;
+  while ((n >> shift) > 4096) ++shift;
+  const int64_t n_b = (n >> shift) + 1;
+  const int64_t nt = nnz > kParallelMin ? std::max(1, omp_get_max_threads()) : 1;
+  const int64_t chunk = cdiv(std::max<int64_t>(nnz, 1), nt);
+  std::vector<int64_t> hist(size_t(nt) * size_t(n_b), 0);
+#pragma omp parallel for schedule(static, 1) if (nt > 1)
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t* h = hist.data() + size_t(t) * size_t(n_b);
+    const int64_t e0 = std::min(nnz, t * chunk), e1 = std::min(nnz, e0 + chunk);
+    for (int64_t e = e0; e < e1; ++e) h[rows[e] >> shift]++;
+  }
+  std::vector<int64_t> bstart(size_t(n_b) + 1, 0);
+  int64_t acc = 0;
+  for (int64_t i = 0; i < n_b; ++i) {
+    bstart[size_t(i)] = acc;
+    for (int64_t t = 0; t < nt; ++t) {
+      int64_t& h = hist[size_t(t) * size_t(n_b) + size_t(i)];
+      const int64_t c = h;
+      h = acc;
+      acc += c;
+    }
+  }
+  bstart[size_t(n_b)] = acc;
+  std::unique_ptr<uint64_t[]> keys(new uint64_t[size_t(std::max<int64_t>(nnz, 1))]);
+  std::unique_ptr<double[]> kval(new double[size_t(std::max<int64_t>(nnz, 1))]);
+#pragma omp parallel for schedule(static, 1) if (nt > 1)
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t* h = hist.data() + size_t(t) * size_t(n_b);
+    const int64_t e0 = std::min(nnz, t * chunk), e1 = std::min(nnz, e0 + chunk);
+    for (int64_t e = e0; e < e1; ++e) {
+      const int64_t d = h[rows[e] >> shift]++;
+      keys[size_t(d)] = (uint64_t(rows[e]) << 32) | uint64_t(cols[e]);
+      kval[size_t(d)] = values[e];
+    }
+  }
+  scol.reset(new int32_t[size_t(std::max<int64_t>(nnz, 1))]);
+  sval.reset(new double[size_t(std::max<int64_t>(nnz, 1))]);
+  rptr.assign(size_t(n) + 1, 0);
+  int cbits = 0;
+  while (cbits < 32 && (int64_t(1) << cbits) < n) ++cbits;
+  constexpr int kRB = 11;
+#pragma omp parallel if (nt > 1)
+  {
+    std::vector<uint64_t> ka, kb;
+    std::vector<double> va, vb;
+    std::vector<int64_t> cnt(size_t(1) << kRB);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t bi = 0; bi < n_b; ++bi) {
+      const int64_t r0 = bi << shift;
+      const int64_t k0 = bstart[size_t(bi)], k1 = bstart[size_t(bi) + 1], nk = k1 - k0;
+      if (nk == 0) continue;
+      ka.assign(keys.get() + k0, keys.get() + k1);
+      va.assign(kval.get() + k0, kval.get() + k1);
+      kb.resize(size_t(nk));
+      vb.resize(size_t(nk));
+      auto pass = [&](int lo, int bits, uint64_t base) {
+        const uint64_t mask = (uint64_t(1) << bits) - 1;
+        std::fill(cnt.begin(), cnt.begin() + (int64_t(1) << bits), 0);
+        for (int64_t k = 0; k < nk; ++k) cnt[size_t(((ka[size_t(k)] - base) >> lo) & mask)]++;
+        int64_t a = 0;
+        for (int64_t i = 0; i < (int64_t(1) << bits); ++i) {
+          const int64_t c = cnt[size_t(i)];
+          cnt[size_t(i)] = a;
+          a += c;
+        }
+        for (int64_t k = 0; k < nk; ++k) {
+          const int64_t d = cnt[size_t(((ka[size_t(k)] - base) >> lo) & mask)]++;
+          kb[size_t(d)] = ka[size_t(k)];
+          vb[size_t(d)] = va[size_t(k)];
+        }
+        ka.swap(kb);
+        va.swap(vb);
+      };
+      for (int lo = 0; lo < cbits; lo += kRB) pass(lo, std::min(kRB, cbits - lo), 0);
+      if (shift > 0) pass(32, shift, uint64_t(r0) << 32);
+      for (int64_t k = 0; k < nk; ++k) {
+        scol[size_t(k0 + k)] = int32_t(uint32_t(ka[size_t(k)]));
+        sval[size_t(k0 + k)] = va[size_t(k)];
+        rptr[size_t(ka[size_t(k)] >> 32) + 1]++;
+      }
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) rptr[size_t(i) + 1] += rptr[size_t(i)];
+}
+
 }  // namespace
 
 // ===================================================================== API
@@ -647,30 +742,10 @@ EHYB_API int ehyb_assemble(int64_t n, int64_t nnz, const int64_t* rows, const in
     const int64_t padded = n_parts * vec;
     const int64_t n_sl = padded / warp;
     const int64_t n_er_sl = n_er ? cdiv(n_er, warp) : 0;
-    // entries grouped by row, then ordered by (original column, entry index):
-    // the order of np.lexsort((cols, rows)) including duplicate coordinates
-    std::vector<int64_t> rptr(size_t(n) + 1, 0);
-    {
-      std::vector<std::atomic<int64_t>> c(size_t(n) + 1);
-#pragma omp parallel for schedule(static) if (n > kParallelMin)
-      for (int64_t i = 0; i <= n; ++i) c[size_t(i)].store(0, std::memory_order_relaxed);
-#pragma omp parallel for schedule(static) if (nnz > kParallelMin)
-      for (int64_t e = 0; e < nnz; ++e) c[size_t(rows[e])].fetch_add(1, std::memory_order_relaxed);
-      for (int64_t i = 0; i < n; ++i) rptr[size_t(i) + 1] = rptr[size_t(i)] + c[size_t(i)].load();
-    }
-    std::vector<int64_t> ent(static_cast<size_t>(nnz));
-    {
-      std::vector<std::atomic<int64_t>> cur(static_cast<size_t>(n));
-#pragma omp parallel for schedule(static) if (n > kParallelMin)
-      for (int64_t i = 0; i < n; ++i) cur[size_t(i)].store(rptr[size_t(i)], std::memory_order_relaxed);
-#pragma omp parallel for schedule(static) if (nnz > kParallelMin)
-      for (int64_t e = 0; e < nnz; ++e)
-        ent[size_t(cur[size_t(rows[e])].fetch_add(1, std::memory_order_relaxed))] = e;
-    }
-#pragma omp parallel for schedule(dynamic, 1024) if (n > kParallelMin)
-    for (int64_t i = 0; i < n; ++i)
-      std::sort(ent.begin() + rptr[size_t(i)], ent.begin() + rptr[size_t(i) + 1],
-                [&](int64_t a, int64_t b) { return cols[a] < cols[b] || (cols[a] == cols[b] && a < b); });
+    std::vector<int64_t> rptr;
+    std::unique_ptr<int32_t[]> scol;
+    std::unique_ptr<double[]> sval;
+    group_rows(n, nnz, rows, cols, values, rptr, scol, sval);
     // row widths
 #pragma omp parallel for schedule(static) if (padded > kParallelMin)
     for (int64_t i = 0; i < padded; ++i) ell_row_widths[i] = 0;
@@ -680,7 +755,7 @@ EHYB_API int ehyb_assemble(int64_t n, int64_t nnz, const int64_t* rows, const in
     for (int64_t r = 0; r < n; ++r) {
       int64_t ni = 0;
       for (int64_t j = rptr[size_t(r)]; j < rptr[size_t(r) + 1]; ++j)
-        ni += assignment[cols[ent[size_t(j)]]] == assignment[r];
+        ni += assignment[scol[size_t(j)]] == assignment[r];
       ell_row_widths[reorder[r]] = int32_t(ni);
       if (arrange[r] >= 0) er_row_widths[arrange[r]] = int32_t(rptr[size_t(r) + 1] - rptr[size_t(r)] - ni);
     }
@@ -732,8 +807,8 @@ EHYB_API int ehyb_assemble(int64_t n, int64_t nnz, const int64_t* rows, const in
       const int64_t slot = arrange[r];
       int64_t ki = 0, ko = 0;
       for (int64_t j = rptr[size_t(r)]; j < rptr[size_t(r) + 1]; ++j) {
-        const int64_t e = ent[size_t(j)];
-        const int64_t c = cols[e];
+        const int64_t c = scol[size_t(j)];
+        const double x = sval[size_t(j)];
         int64_t d;
         if (assignment[c] == assignment[r]) {
           const int64_t loc = reorder[c] - base;
@@ -741,15 +816,15 @@ EHYB_API int ehyb_assemble(int64_t n, int64_t nnz, const int64_t* rows, const in
           d = position_ell[nr / warp] + nr % warp + ki * warp;
           ++ki;
           col_ell[d] = uint16_t(loc);
-          if (tau == 4) static_cast<float*>(val_ell)[d] = float(values[e]);
-          else static_cast<double*>(val_ell)[d] = values[e];
+          if (tau == 4) static_cast<float*>(val_ell)[d] = float(x);
+          else static_cast<double*>(val_ell)[d] = x;
         } else {
           if (slot < 0) { bad.store(2); continue; }
           d = position_er[slot / warp] + slot % warp + ko * warp;
           ++ko;
           col_er[d] = uint32_t(reorder[c]);
-          if (tau == 4) static_cast<float*>(val_er)[d] = float(values[e]);
-          else static_cast<double*>(val_er)[d] = values[e];
+          if (tau == 4) static_cast<float*>(val_er)[d] = float(x);
+          else static_cast<double*>(val_er)[d] = x;
         }
       }
     }

@@ -108,3 +108,28 @@ def test_errors_match_reference_wording():
     with pytest.raises(ValueError, match="parts"):
         E.build_ehyb(m, tau=8, profile=E.DeviceProfile(2, 4, 64),
                      partition=E.random_partition(8, 8, None, seed=0))
+
+
+@pytest.mark.parametrize("tau,n", [(4, 3000), (8, 3000), (8, 20000)])
+def test_duplicate_coordinates_keep_entry_order(tau, n):
+    """Duplicate (row, col) entries in scrambled COO order: the native
+    radix grouping must reproduce np.lexsort((cols, rows)) — duplicates in
+    entry order (format.py:319) — so every parity array equals the oracle's."""
+    from oracle import ehyb_oracle as O
+
+    rng = np.random.default_rng(11)
+    r = rng.integers(0, n, size=40000)
+    c = np.clip(r + rng.integers(-40, 41, size=r.size), 0, n - 1)
+    dup = rng.integers(0, r.size, size=5000)  # repeated coordinates, new values
+    rows = np.concatenate([r, r[dup]]).astype(np.int64)
+    cols = np.concatenate([c, c[dup]]).astype(np.int64)
+    vals = rng.uniform(-1, 1, size=rows.size)
+    perm = rng.permutation(rows.size)
+    rows, cols, vals = rows[perm], cols[perm], vals[perm]
+    profile = (4 if n < 10000 else 16, 32, 48 * 1024)
+    _, _, _, _, _, _, e = product_pipeline(n, rows, cols, vals, tau, profile)
+    s = O.pipeline(n, rows, cols, vals, tau, *profile)
+    for key in ("val_ell", "col_ell", "val_er", "col_er", "position_ell", "width_ell",
+                "position_er", "width_er", "ell_row_widths", "er_row_widths"):
+        got = np.asarray(getattr(e, key))
+        assert got.tobytes() == np.asarray(s[key]).tobytes(), key
