@@ -539,12 +539,26 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
     // parts reduces to the adjacent movable parts (first id on ties).
     int64_t nonfull = 0;
     for (int64_t p = 0; p < n_parts; ++p) nonfull += sizes[p] < capacity;
+    // A vertex whose neighbours all share its part has touched = {a} and
+    // cannot move; that stays true until a neighbour moves. So only boundary
+    // vertices (found in parallel) and later neighbours of moved vertices
+    // are visited — the same decisions in the same order as the full pass.
+    std::vector<uint8_t> active(size_t(n), 0);
+#pragma omp parallel for schedule(dynamic, 4096) if (n > kParallelMin)
+    for (int64_t v = 0; v < n; ++v) {
+      const int32_t a = part[size_t(v)];
+      for (int64_t j = adj_ptr[v]; j < adj_ptr[v + 1]; ++j)
+        if (part[size_t(adj[j])] != a) {
+          active[size_t(v)] = 1;
+          break;
+        }
+    }
     std::vector<int64_t> cnt(size_t(n_parts), 0);
     std::vector<int64_t> touched;
     for (int64_t v = 0; v < n; ++v) {
-      if (v + 8 < n)  // neighbours' assignments of a vertex 8 ahead (random lines)
+      if (v + 8 < n && active[size_t(v + 8)])  // neighbours' parts of a vertex 8 ahead
         for (int64_t j = adj_ptr[v + 8]; j < adj_ptr[v + 9]; ++j) __builtin_prefetch(part.data() + adj[j]);
-      if (adj_ptr[v + 1] == adj_ptr[v]) continue;
+      if (!active[size_t(v)]) continue;
       int64_t a = part[v];
       touched.clear();
       for (int64_t j = adj_ptr[v]; j < adj_ptr[v + 1]; ++j) {
@@ -569,6 +583,8 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
         sizes[best] += 1;
         if (a_was_full && sizes[a] < capacity) ++nonfull;
         if (sizes[best] >= capacity) --nonfull;
+        for (int64_t j = adj_ptr[v]; j < adj_ptr[v + 1]; ++j)
+          if (adj[j] > v) active[size_t(adj[j])] = 1;
       }
     }
 #pragma omp parallel for schedule(static) if (n > kParallelMin)
