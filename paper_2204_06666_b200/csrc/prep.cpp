@@ -212,7 +212,7 @@ void group_rows(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols
   {
     std::vector<uint64_t> ka, kb;
     std::vector<double> va, vb;
-    std::vector<int64_t> cnt(size_t(1) << kRB);
+    std::vector<int64_t> cnt(size_t(1) << std::max(kRB, shift));  // the vertex pass uses shift bits
 #pragma omp for schedule(dynamic, 1)
     for (int64_t bi = 0; bi < n_b; ++bi) {
       const int64_t r0 = bi << shift;
@@ -360,7 +360,7 @@ EHYB_API int ehyb_build_graph(int64_t n, int64_t nnz, const int64_t* rows, const
 #pragma omp parallel if (!serial)
     {
       std::vector<uint64_t> bufa, bufb;
-      std::vector<int64_t> cnt(size_t(1) << kRB);
+      std::vector<int64_t> cnt(size_t(1) << std::max(kRB, shift));  // the vertex pass uses shift bits
 #pragma omp for schedule(dynamic, 1)
       for (int64_t bi = 0; bi < n_b; ++bi) {
         const int64_t v0 = bi << shift, v1 = std::min<int64_t>(n, (bi + 1) << shift);
@@ -459,7 +459,12 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
     fw.init_ones(n_conn);
     int64_t cursor = 0;
 
+    // assigned flags as a bitset (n/8 bytes: L2-resident where the int32
+    // part array is not) for the BFS membership tests
+    std::vector<uint64_t> taken(size_t((n + 63) >> 6), 0);
+    auto is_taken = [&](int64_t v) { return (taken[size_t(v >> 6)] >> (v & 63)) & 1u; };
     auto assign = [&](int64_t v, int64_t pid) {
+      taken[size_t(v >> 6)] |= 1ull << (v & 63);
       part[v] = int32_t(pid);
       sizes[pid] += 1;
       if (pos_of[size_t(v)] >= 0) fw.dec(pos_of[size_t(v)]);
@@ -467,7 +472,7 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
     // partition.py:131-144: first unassigned vertex of minimum degree; when the
     // unassigned part of its equal-degree run holds >1 vertex, draw its index
     auto next_seed = [&]() -> int64_t {
-      while (cursor < n_conn && part[by_degree[size_t(cursor)]] >= 0) ++cursor;
+      while (cursor < n_conn && is_taken(by_degree[size_t(cursor)])) ++cursor;
       if (cursor >= n_conn) return -1;
       int64_t d = adj_ptr[by_degree[size_t(cursor)] + 1] - adj_ptr[by_degree[size_t(cursor)]];
       int64_t run_end = deg_start[size_t(d) + 1];
@@ -495,16 +500,13 @@ EHYB_API int ehyb_partition_graph(int64_t n, const int64_t* adj_ptr, const int32
         if (qh + 8 < qt) __builtin_prefetch(adj + adj_ptr[queue[qh + 8]]);
         if (qh + 4 < qt) {
           const int64_t f = queue[qh + 4];
-          for (int64_t j = adj_ptr[f]; j < adj_ptr[f + 1]; ++j) {
-            __builtin_prefetch(part.data() + adj[j], 1);
-            __builtin_prefetch(pos_of.data() + adj[j]);
-          }
+          for (int64_t j = adj_ptr[f]; j < adj_ptr[f + 1]; ++j) __builtin_prefetch(pos_of.data() + adj[j]);
         }
         int64_t u = queue[qh++];
         bool full = false;
         for (int64_t j = adj_ptr[u]; j < adj_ptr[u + 1]; ++j) {
           int64_t w = adj[j];
-          if (part[w] < 0) {
+          if (!is_taken(w)) {
             assign(w, pid);
             ++grown;
             queue[qt++] = int32_t(w);

@@ -133,3 +133,54 @@ def test_duplicate_coordinates_keep_entry_order(tau, n):
                 "position_er", "width_er", "ell_row_widths", "er_row_widths"):
         got = np.asarray(getattr(e, key))
         assert got.tobytes() == np.asarray(s[key]).tobytes(), key
+
+
+def test_large_dimension_radix_buckets():
+    """n above 2^23 (row buckets of 4096 rows: the in-bucket row pass is wider
+    than the 11-bit column passes). build_graph against np.unique over the
+    symmetric keys (partition.py:92-98) and the SELL slabs against a
+    vectorised restatement of assemble_ehyb's placement (format.py:319-380)."""
+    rng = np.random.default_rng(5)
+    n = (1 << 23) + 4099
+    hubs = rng.integers(0, n, size=4000)
+    rows = np.concatenate([hubs, rng.choice(hubs, 60000)]).astype(np.int64)
+    cols = np.concatenate([hubs, rng.choice(hubs, 60000)]).astype(np.int64)
+    rows = np.concatenate([rows, rows[:5000]])  # duplicate coordinates
+    cols = np.concatenate([cols, cols[:5000]])
+    vals = rng.uniform(-1, 1, size=rows.size)
+    perm = rng.permutation(rows.size)
+    rows, cols, vals = rows[perm], cols[perm], vals[perm]
+    m, params, g, parts, cls, plan, e = product_pipeline(
+        n, rows, cols, vals, 8, (296, 32, 231424))
+    off = rows != cols
+    keys = np.unique(np.concatenate([rows[off] * n + cols[off], cols[off] * n + rows[off]]))
+    assert np.array_equal(g.adj_ptr, np.concatenate([[0], np.cumsum(np.bincount(keys // n, minlength=n))]))
+    assert np.array_equal(g.adj, (keys % n).astype(np.int32))
+
+    C, vec = params.warp_size, params.vec_cache_size
+    asg, reorder, arrange = parts.assignment, plan.reorder_table, plan.arrange_table
+    order = np.lexsort((np.arange(rows.size), cols, rows))
+    r, c, v = rows[order], cols[order], vals[order]
+    inner = asg[r] == asg[c]
+
+    def ranks(rr):
+        return np.arange(rr.size) - np.searchsorted(rr, rr, side="left")
+
+    ri, ci = r[inner], c[inner]
+    nr = reorder[ri]
+    d = e.position_ell[nr // C] + nr % C + ranks(ri) * C
+    want_v = np.zeros_like(e.val_ell)
+    want_c = np.zeros_like(e.col_ell)
+    want_v[d] = v[inner]
+    want_c[d] = reorder[ci] - (nr // vec) * vec
+    assert want_v.tobytes() == e.val_ell.tobytes()
+    assert want_c.tobytes() == e.col_ell.tobytes()
+    ro, co = r[~inner], c[~inner]
+    slot = arrange[ro]
+    d = e.position_er[slot // C] + slot % C + ranks(ro) * C
+    want_v = np.zeros_like(e.val_er)
+    want_c = np.zeros_like(e.col_er)
+    want_v[d] = v[~inner]
+    want_c[d] = reorder[co]
+    assert want_v.tobytes() == e.val_er.tobytes()
+    assert want_c.tobytes() == e.col_er.tobytes()
