@@ -131,6 +131,7 @@ struct ehyb_dev {
   unsigned int* part_flag = nullptr;  // persistent mode: per-partition publication
   int32_t* pool_grp = nullptr;         // pooled-slice range per iteration group
   int32_t pool_groups = 0;
+  int32_t pool_last_scratch = 0;  // last iteration group via scratch + owner add
   unsigned int* pool_gctr = nullptr;
   unsigned int* pool_ctr = nullptr;
   unsigned int* epoch_dev = nullptr;  // [2] launch epoch, CTAs finished (device-side: graph-safe)
@@ -243,6 +244,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_grp = h->pool_grp;
   P.pool_groups = h->pool_groups;
   P.pool_gctr = h->pool_gctr;
+  P.pool_last_scratch = h->pool_last_scratch;
   P.epoch_dev = h->epoch_dev;
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
@@ -270,6 +272,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
     P.pool_lo = P.pool_hi;
     P.pool_own_ptr = nullptr;
     P.part_flag = nullptr;  // no group drains (the group counters still reset)
+    P.pool_last_scratch = 0;
   }
   void (*kern)(const SpmvParams<T>) = (do_ell && h->window_in_smem)
                                            ? spmv_fused_kernel<T, STRICT, C32, true, false>
@@ -893,6 +896,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     if (!pool_gptr.empty()) {
       const int64_t ng = int64_t(pool_gptr.size()) - 1;
       h->pool_groups = int32_t(ng);
+      h->pool_last_scratch = ng > 1 && env_double("EHYB_POOL_LAST_SCRATCH", 0.0) != 0.0;
       CUDA_TRY(upload(&h->pool_grp, pool_gptr.data(), pool_gptr.size() * 4, &h->bytes));
       CUDA_TRY(cudaMalloc(&h->pool_gctr, size_t(ng) * 8 + 16));
       CUDA_TRY(cudaMemset(h->pool_gctr, 0, size_t(ng) * 8 + 16));

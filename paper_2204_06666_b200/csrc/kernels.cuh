@@ -96,6 +96,8 @@ struct SpmvParams {
   const int32_t* __restrict__ pool_grp;  // [n_groups+1] pooled-slice range of each group
   int32_t pool_groups;
   unsigned int* pool_gctr;          // [2][n_groups] group claim counters by epoch
+  int32_t pool_last_scratch;        // 1: the last group is computed early into pool_acc and
+                                    // added by its owners after the loop (no in-place wait)
   unsigned int* epoch_dev;          // [2]: launch sequence number (>= 1), CTAs finished; kept
                                     // on the device so a captured CUDA graph replays correctly
   // own-ER shared-memory buffer (overlap of ER gathers with the ELL stream)
@@ -871,6 +873,33 @@ __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, 
   }
 }
 
+// The last iteration group when pool_last_scratch: its owners run in the
+// final iteration, so finishing in place would leave the whole group to the
+// end of the launch. Instead every slice is computed as soon as a warp claims
+// it (ER-first warps of the last iteration, then anyone after the loop) into
+// the scratch and counted for its owner; the owner CTA adds the sums once
+// its count is complete. Computing never waits.
+template <typename T, bool STRICT>
+__device__ void pool_scratch_group(const SpmvParams<T>& P, int lane, uint32_t ep, int g) {
+  if (g < 0 || g >= P.pool_groups) return;
+  const int64_t lo = __ldg(P.pool_grp + g), hi = __ldg(P.pool_grp + g + 1);
+  if (hi <= lo) return;
+  unsigned int* ctr = P.pool_gctr + (ep & 1u) * uint32_t(P.pool_groups) + uint32_t(g);
+  unsigned int* done = P.pool_done + (ep & 1u) * uint32_t(P.n_parts);
+  for (;;) {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1u);
+    const int64_t s = lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
+    if (s >= hi) break;
+    const ErMeta m = er_claimed_meta(P, s, hi, lane);
+    P.pool_acc[(s - P.pool_lo) * 32 + lane] = er_slice_compute<T, STRICT>(P, m);
+    const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(done + uint32_t(rw0 & kRowMask) / uint32_t(P.vec), 1u);
+  }
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1282,7 +1311,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     // stream; with several partitions per CTA, the group whose owners ran in
     // the previous iteration
     if (!persistent) pool_drain<T, STRICT>(P, lane, 0, ep);
-    else if (P.part_flag) pool_drain_group<T, STRICT>(P, lane, ep, it - 1);
+    else if (P.part_flag) {
+      pool_drain_group<T, STRICT>(P, lane, ep, it - 1);
+      if (P.pool_last_scratch && it == P.pool_groups - 1) pool_scratch_group<T, STRICT>(P, lane, ep, it);
+    }
   }
   const int64_t st_lo = RING ? int64_t(__ldg(P.part_stage_ptr + part)) : 0;
   const int64_t n_st = RING ? int64_t(__ldg(P.part_stage_ptr + part + 1)) - st_lo : 0;
@@ -1484,7 +1516,30 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       while (last + int(gridDim.x) < P.n_parts) last += gridDim.x;
       st_release_gpu(P.part_flag + last, ep);
     }
-    for (int g = 0; g < P.pool_groups; ++g) pool_drain_group<T, STRICT>(P, lane, ep, g);
+    const int g_end = P.pool_last_scratch ? P.pool_groups - 1 : P.pool_groups;
+    for (int g = 0; g < g_end; ++g) pool_drain_group<T, STRICT>(P, lane, ep, g);
+    if (P.pool_last_scratch) {
+      const int gl = P.pool_groups - 1;
+      pool_scratch_group<T, STRICT>(P, lane, ep, gl);
+      const int pl = cta + gl * int(gridDim.x);  // this CTA's partition in the last group
+      if (pl < P.n_parts) {
+        const int32_t q0 = __ldg(P.pool_own_ptr + pl), q1 = __ldg(P.pool_own_ptr + pl + 1);
+        if (q1 > q0) {
+          const unsigned int* done = P.pool_done + (ep & 1u) * uint32_t(P.n_parts) + uint32_t(pl);
+          if (lane == 0)
+            while (ld_acquire_gpu(done) != unsigned(q1 - q0)) __nanosleep(64);
+          __syncwarp();
+          for (int64_t t = wid; t < q1 - q0; t += int64_t(blockDim.x >> 5)) {
+            const int64_t sl = __ldg(P.pool_own_idx + q0 + t);
+            const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
+            if (rw >= 0) {
+              const int64_t r = rw & kRowMask;
+              P.y[r] = add_rn(__ldcg(P.y + r), __ldcg(P.pool_acc + (sl - P.pool_lo) * 32 + lane));
+            }
+          }
+        }
+      }
+    }
   } else if (persistent && P.do_er && P.pool_own_ptr) {
     pool_drain<T, STRICT>(P, lane, 0, ep);
     __syncthreads();
