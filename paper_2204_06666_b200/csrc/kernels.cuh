@@ -1599,6 +1599,7 @@ __global__ void permute_kernel(const T* __restrict__ x_user, const int32_t* __re
 template <typename T>
 __global__ void unpermute_kernel(const T* __restrict__ y_r, const int32_t* __restrict__ reorder,
                                  int64_t n, T* __restrict__ y_user) {
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     y_user[i] = __ldg(y_r + __ldg(reorder + i));
@@ -1618,6 +1619,7 @@ __global__ void dot_partial_kernel(const T* __restrict__ a, const T* __restrict_
                                    double* __restrict__ partial) {
   __shared__ double red[32];
   double s = 0.0;
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     s += double(a[i]) * double(b[i]);
@@ -1658,6 +1660,7 @@ __global__ void cg_xr_kernel(T* __restrict__ x, T* __restrict__ r, const T* __re
   const double alpha = rr[0] / pq[0];
   const T a = T(alpha);
   double s = 0.0;
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     x[i] = x[i] + a * p[i];
@@ -1681,6 +1684,7 @@ __global__ void cg_p_kernel(T* __restrict__ p, const T* __restrict__ r,
                             const double* __restrict__ rr_new, const double* __restrict__ rr_old,
                             int64_t n) {
   const T beta = T(rr_new[0] / rr_old[0]);
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     p[i] = r[i] + beta * p[i];
@@ -1694,6 +1698,7 @@ __global__ void dot2_partial_kernel(const T* __restrict__ a, const T* __restrict
                                     double* __restrict__ partial) {
   __shared__ double red[2][32];
   double s0 = 0.0, s1 = 0.0;
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     s0 += double(a[i]) * double(b[i]);
@@ -1779,6 +1784,7 @@ __global__ void cgcg_update_kernel(T* __restrict__ x, T* __restrict__ r, T* __re
                                    T* __restrict__ s, const T* __restrict__ w,
                                    const double* __restrict__ sc, int64_t n) {
   const T alpha = T(sc[3]), beta = T(sc[4]);
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const T pi = r[i] + beta * p[i];
@@ -1794,6 +1800,7 @@ template <typename T>
 __global__ void axpy_kernel(const double* __restrict__ a, double sign, const T* __restrict__ x,
                             T* __restrict__ y, int64_t n) {
   const T alpha = T(sign * a[0]);
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     y[i] = y[i] + alpha * x[i];
