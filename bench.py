@@ -113,7 +113,8 @@ def build_workload(name: str):
     t_gen = time.perf_counter() - t0
     m = E.CooMatrix(n, n, r, c, v)
     del r, c, v
-    params = E.compute_params(n, tau, E.B200_PROFILE)
+    prof = W.CONFIG_PROFILES.get(name)
+    params = E.compute_params(n, tau, E.DeviceProfile(*prof) if prof else E.B200_PROFILE)
     t0 = time.perf_counter()
     g = E.build_graph(m)
     parts = E.partition_graph(g, params.n_parts, params.vec_cache_size, seed=0)
@@ -163,40 +164,58 @@ def cpu_engine_sample(e, xr, budget_s: float, threads: int):
     return prep, parts, er, y, flops, desc
 
 
+def reference_workload(args):
+    """The workload our arm runs for this N (config name, profile), built by
+    the ORACLE's C restatement of the reference preprocessing — no product
+    code or library on this path."""
+    from paper_2204_06666_b200 import workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    g = max(world, args.gpus)
+    name = args.config if g <= 1 else dist_config_name(args, g)
+    n, r, c, v, tau = W.build_config(name) if name in W.CONFIGS else _weak_matrix(g)
+    profile = W.CONFIG_PROFILES.get(name) or dist_profile(args, g)
+    return name, n, r, c, v, tau, profile
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU SpMV path (engine.py:108-216),
-    restated in C (oracle/ehyb_oracle.c), all host threads, rank 0 only."""
+    """--impl reference: the reference's CPU SpMV path (engine.py:108-216) on
+    the box's host cores. The reference is pure Python (nothing to compile),
+    so per the tier rules the arm times the oracle port: the EHYB arrays come
+    from oracle/ehyb_prep_oracle.c (the C restatement of the reference
+    preprocessing, checked against the reference's own digests), the SpMV
+    from oracle/ehyb_oracle.c with all host threads. Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import paper_2204_06666_b200 as E
-    from paper_2204_06666_b200 import workloads as W
     from golden_util import digest
+    from oracle import c_oracle, c_prep
+    from paper_2204_06666_b200 import workloads as W
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
-        # the workload our arm runs at N GPUs (weak scaling), same profile
-        from paper_2204_06666_b200 import distributed as D
-
-        g = max(world, args.gpus)
-        t0 = time.perf_counter()
-        n, r, c, v = D.weak_config(g)
-        m = E.CooMatrix(n, n, r, c, v)
-        del r, c, v
-        e = E.build_ehyb(m, tau=8, profile=E.b200_profile(g))
-        prep_t = {"build_s": time.perf_counter() - t0}
-        gold = None
-        args.config = f"weak{g}"
-    else:
-        m, e, prep_t = build_workload(args.config)
-        gold = golden_y_digest(args.config)
-    if gold is not None and digest(e.val_ell) != gold["digests"]["val_ell"]:
-        raise SystemExit("reference arm: EHYB arrays differ from the reference's digests")
-    x = W.deterministic_vector(e.dimension, 0)
-    xr = E.permute_vector(x, e.plan)
+    name, n, r, c, v, tau, profile = reference_workload(args)
+    args.config = name
+    prep_t = {}
+    t0 = time.perf_counter()
+    e = c_prep.build_ehyb(n, r, c, v, tau, tuple(profile), timings=prep_t)
+    prep_t["total_s"] = time.perf_counter() - t0
+    nnz = int(r.size)
+    del r, c, v
+    gold = golden_y_digest(name)
+    parity = "no golden record for this config"
+    if gold is not None:
+        if digest(e.val_ell) != gold["digests"]["val_ell"] or \
+                digest(e.col_er) != gold["digests"]["col_er"]:
+            raise SystemExit("reference arm: EHYB arrays differ from the reference's digests")
+        parity = "EHYB arrays == the reference's digests"
+    x = W.deterministic_vector(n, 0)
+    xr = np.zeros(e.padded_dimension, np.float32 if tau == 4 else np.float64)
+    xr[e.plan.reorder_table[:n]] = x
     threads = len(os.sched_getaffinity(0))
     per_step_budget = max(0.05, 120.0 / max(1, args.steps + args.warmup))
     prep, parts, er, y, flops, desc = cpu_engine_sample(e, xr, per_step_budget, threads)
+    if gold is not None and desc == "full product":
+        ok = digest(y) == gold["y_reordered"]
+        parity += "; y == the reference's y digest" if ok else "; y MISMATCH"
     for _ in range(args.warmup):
         prep.spmv(xr, threads, out=y, parts=parts, er_slices=er)
     t0 = time.perf_counter()
@@ -204,46 +223,157 @@ def run_reference(args):
         prep.spmv(xr, threads, out=y, parts=parts, er_slices=er)
     dt = (time.perf_counter() - t0) / args.steps
     value = flops / dt / 1e9
-    desc_full = f"{desc} per step ({flops} flops), C restatement of engine.py spmv_ehyb"
+    desc_full = (f"{desc} per step ({flops} flops); SpMV = oracle/ehyb_oracle.c (C restatement "
+                 f"of engine.py spmv_ehyb, OpenMP), arrays = oracle/ehyb_prep_oracle.c")
+    ref_py = (reference_python_engine(e, xr, name)
+              if not args.no_ref_python and e.dimension <= 6_000_000 else None)
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64" if e.params.tau == 8 else "f32",
-        "data": "synthetic", "config": config_block(args, m, e),
+        "vs_baseline": None, "dtype": "f64" if tau == 8 else "f32",
+        "data": "synthetic", "config": config_block(args, None, e, nnz=nnz),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": desc_full},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "preprocessing_s": prep_t,
+        "parity": parity,
+        "preprocessing_s": dict(prep_t, source="oracle/ehyb_prep_oracle.c (C restatement of the "
+                                               "reference preprocessing), host threads"),
+        "reference_python_preprocessing_s": (gold or {}).get("timings"),
+        "reference_python_engine": ref_py,
+        "repo_libraries_mapped": repo_libraries_mapped(),
     }
     print(json.dumps(out), flush=True)
     return 0
 
 
-def config_block(args, m, e):
+def repo_libraries_mapped():
+    """Shared objects from this repo mapped into the process (the reference
+    arm must show only oracle/ libraries)."""
+    try:
+        with open("/proc/self/maps") as fh:
+            libs = {ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in libs if p.startswith(ROOT))
+
+
+def reference_python_engine(e, xr, name):
+    """One call of the UNMODIFIED reference engine (`ehyb.spmv_ehyb`, the
+    pure-Python simulator installed into baseline/_ref) on the same arrays:
+    how the reference itself runs this path (GIL-bound, ~1 core)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "ehyb")):
+        return {"unavailable": "baseline/_ref not installed"}
+    code = r"""
+import json, sys, time, numpy as np
+sys.path.insert(0, sys.argv[1])
+import ehyb
+d = np.load(sys.argv[2], allow_pickle=False)
+p = ehyb.EhybParams(k=int(d['k']), n_parts=int(d['n_parts']), vec_cache_size=int(d['vec']),
+                    tau=int(d['tau']), warp_size=int(d['warp']))
+plan = ehyb.ReorderPlan(reorder_table=d['reorder'], inverse_table=d['inverse'],
+                        arrange_table=d['arrange'], y_idx_er=d['y_idx_er'],
+                        n_er_rows=int(d['n_er']), dimension=int(d['n']),
+                        padded_dimension=int(d['padded']))
+e = ehyb.EhybMatrix(params=p, plan=plan, dimension=int(d['n']), padded_dimension=int(d['padded']),
+                    val_ell=d['val_ell'], col_ell=d['col_ell'], position_ell=d['position_ell'],
+                    width_ell=d['width_ell'], part_boundary=d['part_boundary'],
+                    ell_row_widths=d['ell_row_widths'], val_er=d['val_er'], col_er=d['col_er'],
+                    position_er=d['position_er'], width_er=d['width_er'],
+                    er_row_widths=d['er_row_widths'])
+t0 = time.perf_counter()
+y, st = ehyb.spmv_ehyb(e, d['xr'], ehyb.ExecutionConfig(worker_count=1))
+dt = time.perf_counter() - t0
+np.save(sys.argv[3], y)
+print(json.dumps({"s": dt, "flops": int(st.flops)}))
+"""
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        arrs = os.path.join(td, "e.npz")
+        p = e.params
+        np.savez(arrs, k=p.k, n_parts=p.n_parts, vec=p.vec_cache_size, tau=p.tau, warp=p.warp_size,
+                 n=e.dimension, padded=e.padded_dimension, n_er=e.plan.n_er_rows,
+                 reorder=e.plan.reorder_table, inverse=e.plan.inverse_table,
+                 arrange=e.plan.arrange_table, y_idx_er=e.plan.y_idx_er, xr=xr,
+                 **{k: getattr(e, k) for k in ("val_ell", "col_ell", "position_ell", "width_ell",
+                                                "part_boundary", "ell_row_widths", "val_er",
+                                                "col_er", "position_er", "width_er",
+                                                "er_row_widths")})
+        yout = os.path.join(td, "y.npy")
+        r = subprocess.run([sys.executable, "-c", code, ref, arrs, yout], capture_output=True,
+                           text=True, timeout=900, env={**os.environ, "PYTHONPATH": ""})
+        if r.returncode != 0:
+            return {"unavailable": r.stderr.strip().splitlines()[-1][:200] if r.stderr else "failed"}
+        res = json.loads(r.stdout.strip().splitlines()[-1])
+        from golden_util import digest
+
+        gold = golden_y_digest(name)
+        y = np.load(yout)
+        return {"value": res["flops"] / res["s"] / 1e9, "unit": UNIT, "s_per_spmv": res["s"],
+                "cores": 1, "api": "ehyb.spmv_ehyb(e, x_r, ExecutionConfig(worker_count=1)) "
+                                   "from baseline/_ref (unmodified reference)",
+                "y_matches_reference_digest": None if gold is None
+                else digest(y) == gold["y_reordered"]}
+
+
+B200_PROFILE = (148, 32, 231424)
+
+
+def dist_config_name(args, g: int) -> str:
+    """The N > 1 workload: cfg5 (BASELINE configs[4], the 27-point 256^3
+    stencil the north star's 8-GPU target is quoted on) unless --config
+    names another; "weak" = the 128*N x 128 x 128 weak-scaling stencil."""
+    return "cfg5" if args.config is None else args.config
+
+
+def dist_profile(args, g: int):
+    """G-independent structure (SURVEY.md 8e option i): every N uses the
+    1-GPU B200 profile, so T_1 and T_N stream identical bytes; only the
+    weak-scaling workload grows its partitions with N."""
+    name = dist_config_name(args, g)
+    if name == "weak":
+        return (148 * g, 32, B200_PROFILE[2])
+    from paper_2204_06666_b200 import workloads as W
+
+    return W.CONFIG_PROFILES.get(name, B200_PROFILE)
+
+
+def _weak_matrix(g: int):
+    from paper_2204_06666_b200 import workloads as W
+
+    n, r, c, v = W.permute_symmetric(*W.stencil27(128 * g, 128, 128), seed=1)
+    return n, r, c, v, 8
+
+
+def min_bytes_of(e) -> int:
+    """SURVEY.md 8d minimum-bytes model: nnz_ell*(tau+2) + nnz_er*(tau+4) + 2*n*tau."""
+    t = e.params.tau
+    return int(e.nnz_ell * (t + 2) + e.nnz_er * (t + 4) + 2 * e.dimension * t)
+
+
+def config_block(args, m, e, nnz=None):
     from paper_2204_06666_b200 import workloads as W
 
     desc = (W.CONFIGS[args.config][0] if args.config in W.CONFIGS else
             f"27-point stencil {e.dimension // (128 * 128)}x128x128, random symmetric "
-            f"permutation (the {args.config[4:]}-GPU weak-scaling workload)")
+            f"permutation (the weak-scaling workload)")
+    p = e.params
+    prof = W.CONFIG_PROFILES.get(args.config, (p.n_parts // max(1, p.k), p.warp_size,
+                                               B200_PROFILE[2]))
     return {
         "workload": f"{args.config}: {desc}",
-        "n": int(e.dimension), "nnz": int(m.nnz), "tau": int(e.params.tau),
-        "profile": f"DeviceProfile({e.params.n_parts // max(1, e.params.k)}, 32, 231424)",
-        "n_parts": int(e.n_parts), "vec_cache_size": int(e.params.vec_cache_size),
+        "n": int(e.dimension), "nnz": int(m.nnz if m is not None else nnz), "tau": int(p.tau),
+        "profile": f"DeviceProfile{tuple(prof)}", "k": int(p.k),
+        "n_parts": int(e.n_parts), "vec_cache_size": int(p.vec_cache_size),
         "nnz_ell": int(e.nnz_ell), "nnz_er": int(e.nnz_er),
         "l2_policy": ("inputs larger than L2 (matrix stream per step >= 2x the 126 MB L2)"
-                      if _min_bytes(e) >= 2 * 126e6 else
+                      if min_bytes_of(e) >= 2 * 126e6 else
                       "L2 flushed (512 MB write) before every timed step; L2-resident "
                       "time reported separately"),
         "parallelism": f"one CTA per partition x{e.n_parts}",
     }
-
-
-def _min_bytes(e):
-    from paper_2204_06666_b200 import min_bytes
-
-    return min_bytes(e)
 
 
 def run_gpu(args):
@@ -302,6 +432,15 @@ def run_gpu(args):
     t_resident = None
     with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
+        # sustained load window (untimed) so the 20 ms nvidia-smi samples see
+        # the kernel running: the timed region alone can be a few ms
+        t_load = time.perf_counter()
+        n_load = 0
+        while time.perf_counter() - t_load < 1.5:
+            for _ in range(64):
+                dm.spmv(xr, y, fma=args.fma, stream=stream)
+            n_load += 64
+            stream.synchronize()
         if flush_l2:
             scratch = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -508,8 +647,15 @@ def run_gpu(args):
                 "sync_call": {"value": flops / t_sync / 1e9, "ms_per_step": t_sync * 1e3,
                               "api": "DeviceMatrix.spmv_host(x, user_order=True) per step "
                                      "(spmv_ehyb_user host path), synchronous"}},
+        "e2e_single_call": {"value": flops / t_sync / 1e9, "unit": UNIT,
+                            "ms_per_step": t_sync * 1e3,
+                            "h2d_bytes_per_step": int(e.dimension * tb),
+                            "d2h_bytes_per_step": int(e.dimension * tb),
+                            "api": "spmv_ehyb_user host path (DeviceMatrix.spmv_host), one "
+                                   "synchronous call per vector"},
         "gpu_launches": args.steps,
-        "clocks": clocks.summary(),
+        "clocks": dict(clocks.summary(), window=f"{n_load} untimed load steps (>= 1.5 s) "
+                                                f"then the timed steps"),
         "parity": parity,
         "cusparse": cus,
         "kernel": {"avg_us": t_step * 1e6, "effective_gbs": achieved,
@@ -530,7 +676,11 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default=None,
+                    help="workload (default: cfg2 at N=1, cfg5 at N>1; 'weak' = weak scaling)")
+    ap.add_argument("--no-ref-python", action="store_true",
+                    help="reference arm: skip the one timed call of the unmodified reference "
+                         "engine from baseline/_ref (~6 s per cfg2 SpMV; skipped above 6M rows)")
     ap.add_argument("--fma", action="store_true", help="fused multiply-add mode")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
@@ -542,6 +692,9 @@ def main(argv=None):
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
     sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None and max(world, args.gpus) <= 1 and not args.dist:
+        args.config = "cfg2"
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

@@ -234,7 +234,10 @@ typedef struct ehyb_csr ehyb_csr;
 EHYB_API int ehyb_csr_create(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
                              const int64_t* col_idx, const double* values, int32_t tau,
                              int device, ehyb_csr** out);
-/* y = A x with cusparseSpMV; alg 1 = CUSPARSE_SPMV_CSR_ALG1, 2 = ALG2. */
+/* y = A x. alg 0 = the reference oracle's own order (replaces
+ * engine.py:56-69 spmv_csr: fp64 products, np.add.reduceat row sums with
+ * numpy's pairwise summation; bitwise the reference's y; tau must be 8);
+ * alg 1 = cusparseSpMV CUSPARSE_SPMV_CSR_ALG1, 2 = ALG2 (the comparator). */
 EHYB_API int ehyb_csr_spmv(ehyb_csr* h, const void* x_dev, void* y_dev, int alg, void* stream);
 EHYB_API int ehyb_csr_destroy(ehyb_csr* h);
 
@@ -276,7 +279,12 @@ EHYB_API int ehyb_dev_spmv_er(ehyb_dev* h, const void* x_ext, void* y_local, int
  * per SpMV. ehyb_dev_spmv_p2p then runs ELL, local ER, the halo pull from
  * peer memory and the halo rows in one launch; it returns (stream-ordered)
  * only after the peers have pulled from this rank, so the next kernel may
- * overwrite x_ext. All ranks must issue the same sequence of p2p SpMVs. */
+ * overwrite x_ext. All ranks must issue the same sequence of p2p SpMVs (in
+ * lockstep: the n-th call on every rank is the same SpMV). A rank whose peer
+ * never issues its matching call does not hang: each cross-rank wait traps
+ * after EHYB_SPIN_TIMEOUT_S seconds (default 20), failing the launch with a
+ * CUDA error, and a launch that fails to issue leaves the sequence number
+ * unchanged. */
 EHYB_API int ehyb_dev_p2p_alloc(ehyb_dev* h, void** x_ext, void** flags);
 EHYB_API int ehyb_ipc_handle(const void* dev_ptr, void* out_handle /* 64 bytes */);
 EHYB_API int ehyb_ipc_open(const void* handle, int device, void** out_ptr);

@@ -1,7 +1,9 @@
 """ORACLE — test / CPU-baseline infrastructure only. NOT part of the product.
 
 ctypes wrapper around oracle/ehyb_oracle.c (the C restatement of the
-reference engine.py:108-216), built with gcc into oracle/_build/.
+reference engine.py:108-216) and oracle/ehyb_prep_oracle.c (the C
+restatement of the reference preprocessing, partition.py:77-204 and
+format.py:123-409), built with gcc into oracle/_build/.
 """
 
 from __future__ import annotations
@@ -13,18 +15,19 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = os.path.join(HERE, "ehyb_oracle.c")
+SRCS = [os.path.join(HERE, "ehyb_oracle.c"), os.path.join(HERE, "ehyb_prep_oracle.c")]
 LIB = os.path.join(HERE, "_build", "libehyb_oracle.so")
 
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= os.path.getmtime(SRC):
+    if not force and os.path.exists(LIB) and all(
+            os.path.getmtime(LIB) >= os.path.getmtime(s) for s in SRCS):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     cmd = ["gcc", "-O3", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
-           "-shared", "-fPIC", SRC, "-o", LIB + ".tmp"]
+           "-shared", "-fPIC", *SRCS, "-o", LIB + ".tmp"]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
@@ -33,8 +36,7 @@ def build(force: bool = False) -> str:
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            build()
+        build()
         h = C.CDLL(LIB)
         vp = C.c_void_p
         for name in ("oracle_spmv_ehyb_f64", "oracle_spmv_ehyb_f32"):

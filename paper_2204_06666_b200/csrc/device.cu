@@ -146,6 +146,13 @@ struct ehyb_dev {
   int32_t* st_chunks = nullptr;
   uint2* ch_stage = nullptr;
   int ell_ahead = 1, er_ahead = 1;
+  // ER padding column (SURVEY.md 8a gotcha 4): x index of the column the
+  // reference's padding slots hold; shards without it locally fix up later
+  int64_t er_pad_idx = 0;
+  int32_t* padfix_rows = nullptr;
+  int64_t padfix_n = 0;
+  unsigned long long spin_timeout_ns = 20000000000ull;  // cross-rank waits trap after this
+  bool cooperative = true;  // launch the fused kernel cooperatively (EHYB_COOPERATIVE=0: plain)
   // long rows (derived): masked out of the slice paths, computed by warps
   uint32_t* long_bits = nullptr;
   int32_t lr_tasks = 0, lr_segs = 0;
@@ -176,7 +183,7 @@ struct ehyb_dev {
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
                     lr_row, lr_padcol, lr_val, lr_col, lr_seg, lr_task_seg, lr_task_nell,
-                    lr_part, lr_cnt, lr_ctr};
+                    lr_part, lr_cnt, lr_ctr, padfix_rows};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (int b = 0; b < kPipe; ++b) {
@@ -213,6 +220,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.er_val = static_cast<const T*>(h->er_val);
   P.er_col = h->er_col;
   P.x = static_cast<const T*>(x);
+  P.er_pad_idx = h->er_pad_idx;
   P.y = static_cast<T*>(y);
   P.vec = h->vec;
   P.warp = int32_t(h->warp);
@@ -239,6 +247,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.peer_flags = h->peer_flags_dev;
   P.my_flags = h->p2p_flags;
   P.seq = h->p2p_seq;
+  P.spin_timeout_ns = h->spin_timeout_ns;
   P.served_per_spmv = h->served_per_spmv;
   P.part_flag = h->part_flag;
   P.pool_grp = h->pool_grp;
@@ -323,8 +332,22 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   const int64_t n_local_parts = h->local_rows / h->vec;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(n_local_parts, h->max_ctas));
 
-  kern<<<dim3(unsigned(grid)), dim3(unsigned(h->threads)), smem, st>>>(P);
-  return cudaGetLastError();
+  // cooperative launch: the runtime guarantees every CTA of the grid is
+  // resident at once (or fails the launch) — the pool, persistent-group and
+  // P2P protocols spin on flags other CTAs write, so a partially scheduled
+  // grid (another kernel holding SMs, e.g. an overlapped NCCL collective)
+  // must never start
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(h->threads));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = h->cooperative ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
 template <typename T>
@@ -340,8 +363,20 @@ cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, boo
 
 cudaError_t launch_spmv(ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
                         cudaStream_t st) {
-  return h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
-                     : launch_mode<double>(h, x, y, mode, ell, er, st);
+  cudaError_t e = h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
+                              : launch_mode<double>(h, x, y, mode, ell, er, st);
+  if (e != cudaSuccess || !er || h->padfix_n == 0) return e;
+  // ER finished: the padding products of rows whose padding column is remote
+  const int blocks = int(std::min<int64_t>((h->padfix_n + 255) / 256, int64_t(h->sm_count) * 4));
+  if (h->tau == 4)
+    pad_fixup_kernel<float><<<blocks, 256, 0, st>>>(static_cast<float*>(y), h->padfix_rows,
+                                                     h->padfix_n,
+                                                     static_cast<const float*>(x) + h->er_pad_idx);
+  else
+    pad_fixup_kernel<double><<<blocks, 256, 0, st>>>(static_cast<double*>(y), h->padfix_rows,
+                                                      h->padfix_n,
+                                                      static_cast<const double*>(x) + h->er_pad_idx);
+  return cudaGetLastError();
 }
 
 double env_double(const char* name, double dflt) {
@@ -350,25 +385,39 @@ double env_double(const char* name, double dflt) {
   return std::atof(v);
 }
 
-// resident CTAs per SM of the fused kernel for this handle's configuration
+template <typename T, bool STRICT>
+const void* fused_variant(bool c32, bool smem) {
+  return c32 ? (smem ? (const void*)spmv_fused_kernel<T, STRICT, true, true, false>
+                     : (const void*)spmv_fused_kernel<T, STRICT, true, false, false>)
+             : (smem ? (const void*)spmv_fused_kernel<T, STRICT, false, true, false>
+                     : (const void*)spmv_fused_kernel<T, STRICT, false, false, false>);
+}
+
+// resident CTAs per SM of the fused kernel for this handle's configuration:
+// the minimum over the strict and FMA variants, so every launch mode fits
+// the one grid the persistent-group layout was built for
 cudaError_t occupancy(const ehyb_dev* h, int* per_sm) {
   const bool c32 = h->warp == 32;
-  const void* k;
-  if (h->tau == 4)
-    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, true, true, false>
-                                 : (const void*)spmv_fused_kernel<float, true, true, false, false>)
-            : (h->window_in_smem ? (const void*)spmv_fused_kernel<float, true, false, true, false>
-                                 : (const void*)spmv_fused_kernel<float, true, false, false, false>);
-  else
-    k = c32 ? (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, true, true, false>
-                                 : (const void*)spmv_fused_kernel<double, true, true, false, false>)
-            : (h->window_in_smem ? (const void*)spmv_fused_kernel<double, true, false, true, false>
-                                 : (const void*)spmv_fused_kernel<double, true, false, false, false>);
-  if (h->smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
-    if (e != cudaSuccess) return e;
+  const void* ks[2];
+  if (h->tau == 4) {
+    ks[0] = fused_variant<float, true>(c32, h->window_in_smem);
+    ks[1] = fused_variant<float, false>(c32, h->window_in_smem);
+  } else {
+    ks[0] = fused_variant<double, true>(c32, h->window_in_smem);
+    ks[1] = fused_variant<double, false>(c32, h->window_in_smem);
   }
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k, h->threads, h->smem);
+  *per_sm = 1 << 30;
+  for (const void* k : ks) {
+    if (h->smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
+      if (e != cudaSuccess) return e;
+    }
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, h->threads, h->smem);
+    if (e != cudaSuccess) return e;
+    *per_sm = std::min(*per_sm, n);
+  }
+  return cudaSuccess;
 }
 
 int grid_for(int64_t n, int threads, int sms) {
@@ -514,6 +563,26 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::unordered_map<int64_t, int64_t> halo_index;
   halo_index.reserve(size_t(n_halo) * 2 + 1);
   for (int64_t i = 0; i < n_halo; ++i) halo_index[halo_cols[i]] = h->local_rows + i;
+  // the ER padding column: what the reference's padding slots hold (global
+  // column 0, format.py:379-380; a renumbered shard layout moves it). A
+  // handle that owns it multiplies it inline (kPadFlag); a shard that does
+  // not reads it from its halo in the fix-up pass after the ER phase
+  int64_t pad_col = -1;
+  for (int64_t j = 0; j < m->n_er_rows; ++j)
+    if (m->er_row_widths[j] < m->width_er[j / C]) {
+      pad_col = m->col_er[int64_t(m->position_er[j / C]) + j % C + C * int64_t(m->er_row_widths[j])];
+      break;
+    }
+  const bool pad_local = pad_col < 0 || (pad_col >= row_lo && pad_col < row_hi);
+  std::vector<int32_t> padfix;
+  if (pad_col >= 0) {
+    if (pad_local) {
+      h->er_pad_idx = pad_col - row_lo;
+    } else {
+      auto it = halo_index.find(pad_col);
+      h->er_pad_idx = it == halo_index.end() ? -1 : it->second;
+    }
+  }
   // launch configuration first: the ER pool is only safe when every CTA of
   // the grid is resident at once (pool rows wait on other CTAs' ELL chunks)
   int optin = 0;
@@ -535,6 +604,8 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   int per_sm = 0;
   CUDA_TRY(occupancy(h.get(), &per_sm));
   h->max_ctas = std::max<int64_t>(1, int64_t(per_sm) * h->sm_count);
+  h->cooperative = env_double("EHYB_COOPERATIVE", 1.0) != 0.0;
+  h->spin_timeout_ns = (unsigned long long)(env_double("EHYB_SPIN_TIMEOUT_S", 20.0) * 1e9);
   // the launch never exceeds one resident wave, so pooled rows (which wait on
   // other CTAs' ELL publication) cannot deadlock
   const bool pool_ok = true;
@@ -724,7 +795,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       const int64_t ref_w = m->width_er[j / C];
       const int64_t lr = m->y_idx_er[j] - row_lo;
       int32_t row = int32_t(lr);
-      if (!shard && w < ref_w) row |= kPadFlag;
+      if (w < ref_w) {
+        if (pad_local) row |= kPadFlag;
+        else padfix.push_back(int32_t(lr));
+      }
       erows[size_t(sl) * 32 + (i - ref.i0)] = row;
       elwidth[size_t(sl) * 32 + (i - ref.i0)] = w;
       eswidth[size_t(sl)] = std::max(eswidth[size_t(sl)], w);
@@ -812,7 +886,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       if (auto it = long_er.find(r); it != long_er.end()) {
         const int64_t j = it->second;
         flags |= kLrHasEr;
-        if (!shard && t.n_er < m->width_er[j / C]) flags |= kLrErPad;
+        if (t.n_er < m->width_er[j / C]) {
+          if (pad_local) flags |= kLrErPad;
+          else padfix.push_back(int32_t(r - row_lo));
+        }
         const int64_t src0 = int64_t(m->position_er[j / C]) + j % C;
         for (int64_t k = 0; k < t.n_er; ++k, ++at) {
           const int64_t src = src0 + C * k;
@@ -859,6 +936,13 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(cudaMalloc(&h->lr_ctr, 16));
     CUDA_TRY(cudaMemset(h->lr_ctr, 0, 16));
     h->bytes += size_t(std::max<int32_t>(h->lr_segs, 1)) * tb + size_t(n_t) * 4 + 16;
+  }
+
+  if (!padfix.empty()) {
+    if (h->er_pad_idx < 0) return fail("ER padding column missing from the shard halo plan");
+    std::sort(padfix.begin(), padfix.end());
+    h->padfix_n = int64_t(padfix.size());
+    CUDA_TRY(upload(&h->padfix_rows, padfix.data(), padfix.size() * 4, &h->bytes));
   }
 
   // ---- permutation tables (int32) for the user-order entry points
@@ -1258,11 +1342,14 @@ EHYB_API int ehyb_dev_spmv_p2p(ehyb_dev* h, void* y_local, int mode, void* strea
     if (!h || !h->p2p_ready) return fail("p2p exchange not set up (ehyb_dev_p2p_setup)");
     if (!y_local) return fail("null argument");
     DeviceGuard guard(h->device);
+    // the sequence number advances only with a launch that was issued: a
+    // failed launch must not put this rank out of step with its peers
     h->p2p_seq += 1;
     h->p2p_active = true;
     const cudaError_t e = launch_spmv(h, h->p2p_x, y_local, mode, true, true,
                                       static_cast<cudaStream_t>(stream));
     h->p2p_active = false;
+    if (e != cudaSuccess) h->p2p_seq -= 1;
     CUDA_TRY(e);
     return 0;
   }
@@ -1480,6 +1567,17 @@ EHYB_API int ehyb_csr_spmv(ehyb_csr* h, const void* x_dev, void* y_dev, int alg,
   EHYB_TRY {
     if (!h) return fail("null handle");
     DeviceGuard guard(h->device);
+    if (alg == 0) {  // the reference's own summation order (engine.py:56-69), fp64
+      if (h->tau != 8) return fail("reference-order CSR product needs float64 values");
+      const int threads = 256;
+      const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((h->n_rows + threads - 1) / threads,
+                                                                     int64_t(1) << 20));
+      csr_ref_kernel<<<unsigned(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+          h->row_ptr, h->col_idx, static_cast<const double*>(h->vals),
+          static_cast<const double*>(x_dev), h->n_rows, static_cast<double*>(y_dev));
+      CUDA_TRY(cudaGetLastError());
+      return 0;
+    }
     const cudaDataType dt = h->tau == 4 ? CUDA_R_32F : CUDA_R_64F;
     cusparseDnVecDescr_t vx, vy;
     CUSPARSE_TRY(cusparseCreateDnVec(&vx, h->n_cols, const_cast<void*>(x_dev), dt));

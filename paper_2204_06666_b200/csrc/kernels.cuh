@@ -55,6 +55,8 @@ struct SpmvParams {
   const T* __restrict__ er_val;
   const uint32_t* __restrict__ er_col;
   const T* __restrict__ x;  // reordered (or [owned | halo]) input
+  int64_t er_pad_idx;       // x index of the column the reference's ER padding slots hold
+                            // (global column 0; kPadFlag rows multiply it once)
   T* __restrict__ y;        // reordered (or owned) output
   int64_t vec;
   int32_t warp;             // slice height C of the ELL body
@@ -88,6 +90,8 @@ struct SpmvParams {
   unsigned long long* my_flags;           // {ready seq, served (cum.), pulled (cum.)}
   unsigned long long seq;                 // SpMV sequence number (>= 1)
   unsigned long long served_per_spmv;     // values peers pull from this rank per SpMV
+  unsigned long long spin_timeout_ns;     // a cross-rank wait longer than this traps (a peer
+                                          // out of lockstep or dead): the launch fails loudly
   // several partitions per CTA: pooled slices grouped by the iteration in
   // which their owner partition runs (p / grid); group g is drained by the
   // ER-first warps during iteration g+1, rows finished in place once the
@@ -547,7 +551,7 @@ __device__ __forceinline__ T er_slice_compute(const SpmvParams<T>& P, const ErMe
     for (int u = 0; u < kUnroll; ++u)
       if (k + u < m.lw) acc = madd<STRICT>(acc, v[u], xv[u]);
   }
-  if (m.rw >= 0 && (m.rw & kPadFlag)) acc = add_rn(acc, mul_rn(T(0), __ldg(P.x)));
+  if (m.rw >= 0 && (m.rw & kPadFlag)) acc = add_rn(acc, mul_rn(T(0), __ldg(P.x + P.er_pad_idx)));
   return acc;
 }
 
@@ -593,8 +597,8 @@ __device__ __forceinline__ void er_pair_compute(const SpmvParams<T>& P, const Er
       if (k + u < b.lw) acc_b = madd<STRICT>(acc_b, vb[u], xb[u]);
     }
   }
-  if (a.rw >= 0 && (a.rw & kPadFlag)) acc_a = add_rn(acc_a, mul_rn(T(0), __ldg(P.x)));
-  if (b.rw >= 0 && (b.rw & kPadFlag)) acc_b = add_rn(acc_b, mul_rn(T(0), __ldg(P.x)));
+  if (a.rw >= 0 && (a.rw & kPadFlag)) acc_a = add_rn(acc_a, mul_rn(T(0), __ldg(P.x + P.er_pad_idx)));
+  if (b.rw >= 0 && (b.rw & kPadFlag)) acc_b = add_rn(acc_b, mul_rn(T(0), __ldg(P.x + P.er_pad_idx)));
 }
 
 // ------------------------------------------------------------- long rows
@@ -699,7 +703,7 @@ __device__ __forceinline__ T long_finish(const SpmvParams<T>& P, int task, T ell
   const int32_t rw = __ldg(P.lr_row + task);
   if (rw & kLrEllPad) ell = add_rn(ell, mul_rn(T(0), __ldg(P.x + __ldg(P.lr_padcol + task))));
   if (!(rw & kLrHasEr)) return ell;
-  if (rw & kLrErPad) er = add_rn(er, mul_rn(T(0), __ldg(P.x)));
+  if (rw & kLrErPad) er = add_rn(er, mul_rn(T(0), __ldg(P.x + P.er_pad_idx)));
   return add_rn(ell, er);
 }
 
@@ -914,6 +918,12 @@ __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsign
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Cross-rank waits (P2P) depend on other processes launching their matching
+// SpMV; if one never does, trap instead of hanging every rank.
+__device__ __forceinline__ void spin_check(unsigned long long t0, unsigned long long limit) {
+  if (globaltimer() - t0 > limit) __trap();
+}
+
 // P2P halo pull of one warp: halo slots [lo, hi) (grouped by source peer)
 // read from the peers' x once each peer has published this SpMV's x; then
 // the pulled values are counted for the peers (served: they may overwrite x)
@@ -926,8 +936,13 @@ __device__ void p2p_pull(const SpmvParams<T>& P, int lane, int64_t lo, int64_t h
     const int src = __ldg(P.pull_src + i);
     int64_t j = i;  // end of this peer's run
     while (j < hi && __ldg(P.pull_src + j) == src) ++j;
-    if (lane == 0)
-      while (ld_acquire_sys_u64(P.peer_flags[src]) < P.seq) __nanosleep(100);
+    if (lane == 0) {
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_sys_u64(P.peer_flags[src]) < P.seq) {
+        __nanosleep(100);
+        spin_check(t0, P.spin_timeout_ns);
+      }
+    }
     __syncwarp();
     const T* px = P.peer_x[src];
     for (int64_t k = i + lane; k < j; k += 32) x_ext[P.local_rows + k] = px[__ldg(P.pull_off + k)];
@@ -1101,9 +1116,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   }
   auto wait_halo = [&]() {  // every halo value of this SpMV is in x_ext
     if constexpr (!P2P) return;
-    if (lane == 0)
-      while (ld_acquire_gpu_u64(P.my_flags + 2) < P.seq * (unsigned long long)P.n_halo)
+    if (lane == 0) {
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire_gpu_u64(P.my_flags + 2) < P.seq * (unsigned long long)P.n_halo) {
         __nanosleep(64);
+        spin_check(t0, P.spin_timeout_ns);
+      }
+    }
     __syncwarp();
   };
   // long rows first (warp 0 of every CTA): their serial chains are the
@@ -1572,7 +1591,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   if (P2P && cta == 0 && threadIdx.x == 0) {
     // this rank's x may be overwritten by the next stream operation only
     // once every peer has pulled its halo values from it
-    while (ld_acquire_sys_u64(P.my_flags + 1) < P.seq * P.served_per_spmv) __nanosleep(100);
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys_u64(P.my_flags + 1) < P.seq * P.served_per_spmv) {
+      __nanosleep(100);
+      spin_check(t0, P.spin_timeout_ns);
+    }
   }
   if (threadIdx.x == 0) {
     if (P.timing) P.timing[8 * cta + 3] = globaltimer();
@@ -1585,10 +1608,120 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   }
 }
 
+// Shards whose x does not hold the ER padding column (global column 0 lives
+// on another rank): their ER rows skip the reference's padding products
+// 0*x[0] in the launch, and this pass applies them once the halo (which then
+// carries that column) is in. z = 0*x[pad] is -0.0, +0.0 or NaN; adding it
+// to the row's ER sum before y = y_ell + er_sum changes y only if z is NaN
+// (y becomes NaN) or z is +0.0 and y came out -0.0 (both terms -0.0: the
+// reference gets +0.0). Exact for every x, one read of z per thread.
+template <typename T>
+__global__ void pad_fixup_kernel(T* __restrict__ y, const int32_t* __restrict__ rows, int64_t n,
+                                 const T* __restrict__ xpad) {
+  const T z = mul_rn(T(0), __ldg(xpad));
+  const bool is_nan = z != z;
+  if (!is_nan && signbit(z)) return;  // -0.0 is the identity of the add
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t r = __ldg(rows + i);
+    const T v = y[r];
+    if (is_nan) y[r] = add_rn(v, z);
+    else if (v == T(0) && signbit(v)) y[r] = T(0);
+  }
+}
+
+// ------------------------------------------- CSR product, reference order
+// The reference oracle spmv_csr (engine.py:56-69): fp64 products
+// v[j] * x[c[j]], then np.add.reduceat over each non-empty row. numpy's
+// reduce loop seeds the row sum with its first product and adds the pairwise
+// sum of the rest (numpy's pairwise_sum: < 8 terms sequential from -0.0,
+// <= 128 terms in 8 strided accumulators combined as a fixed tree plus a
+// sequential tail, longer runs split at n/2 rounded down to a multiple of 8).
+// Reproduced term for term, so y is bitwise the reference's.
+__device__ __forceinline__ double csr_term(const double* __restrict__ v,
+                                           const int32_t* __restrict__ c,
+                                           const double* __restrict__ x, int64_t j) {
+  return __dmul_rn(__ldg(v + j), __ldg(x + __ldg(c + j)));
+}
+
+__device__ double csr_pairwise(const double* __restrict__ v, const int32_t* __restrict__ c,
+                               const double* __restrict__ x, int64_t a, int64_t n) {
+  // iterative form of the recursion: an explicit stack of pending right
+  // halves and of finished left sums (depth <= 2 log2(n / 128) + 2)
+  struct Frame {
+    int64_t a, n;
+    int state;  // 0: not started, 1: left done (sum in `left`)
+    double left;
+  };
+  Frame st[64];
+  int sp = 0;
+  st[0] = {a, n, 0, 0.0};
+  double ret = 0.0;
+  for (;;) {
+    Frame& f = st[sp];
+    if (f.n > 128 && f.state == 0) {
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      f.state = 1;
+      st[sp + 1] = {f.a, n2, 0, 0.0};
+      ++sp;
+      continue;
+    }
+    if (f.n > 128 && f.state == 1) {  // left half finished in `ret`
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      f.left = ret;
+      f.state = 2;
+      st[sp + 1] = {f.a + n2, f.n - n2, 0, 0.0};
+      ++sp;
+      continue;
+    }
+    if (f.n > 128) {  // state 2: right half finished in `ret`
+      ret = __dadd_rn(f.left, ret);
+    } else if (f.n < 8) {
+      double res = -0.0;
+      for (int64_t i = 0; i < f.n; ++i) res = __dadd_rn(res, csr_term(v, c, x, f.a + i));
+      ret = res;
+    } else {
+      double r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = csr_term(v, c, x, f.a + u);
+      int64_t i = 8;
+      for (; i < f.n - (f.n % 8); i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = __dadd_rn(r[u], csr_term(v, c, x, f.a + i + u));
+      }
+      double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < f.n; ++i) res = __dadd_rn(res, csr_term(v, c, x, f.a + i));
+      ret = res;
+    }
+    if (sp == 0) return ret;
+    --sp;
+  }
+}
+
+// one thread per row; empty rows are 0.0 (the reference's np.zeros)
+__global__ void csr_ref_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                               const double* __restrict__ val, const double* __restrict__ x,
+                               int64_t n_rows, double* __restrict__ y) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
+    double s = 0.0;
+    if (b > a) {
+      s = csr_term(val, col, x, a);
+      if (b - a > 1) s = __dadd_rn(s, csr_pairwise(val, col, x, a + 1, b - a - 1));
+    }
+    y[r] = s;
+  }
+}
+
 // ---------------------------------------------------------- vector kernels
 template <typename T>
 __global__ void permute_kernel(const T* __restrict__ x_user, const int32_t* __restrict__ inverse,
                                int64_t n, int64_t padded, T* __restrict__ x_r) {
+  #pragma unroll 4  // independent iterations: loads of 4 elements in flight per thread
   for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < padded;
        j += int64_t(gridDim.x) * blockDim.x) {
     const int64_t src = __ldg(inverse + j);

@@ -42,9 +42,29 @@ def part_range(n_parts: int, world: int, rank: int):
     return p0, p0 + base + (1 if rank < extra else 0)
 
 
+def er_pad_column(e: EhybMatrix) -> int:
+    """The column the reference's ER padding slots hold (global column 0,
+    format.py:379-380; moved by renumber_partitions), or -1 without ER
+    padding. Rows with padding multiply x at this column once (0*x[col])."""
+    warp = e.params.warp_size
+    w = np.asarray(e.er_row_widths, np.int64)
+    if w.size == 0:
+        return -1
+    sw = np.asarray(e.width_er, np.int64)[np.arange(w.size) // warp]
+    j = np.flatnonzero(w < sw)
+    if j.size == 0:
+        return -1
+    j = int(j[0])
+    return int(e.col_er[int(e.position_er[j // warp]) + j % warp + warp * int(w[j])])
+
+
 def halo_columns(e: EhybMatrix, p0: int, p1: int) -> np.ndarray:
     """Sorted distinct global (new-order) columns outside [p0*vec, p1*vec)
-    referenced by the real entries of the ER rows that [p0, p1) owns."""
+    referenced by the real entries of the ER rows that [p0, p1) owns, plus
+    the ER padding column when an owned row has padding slots and another
+    rank owns that column (the reference's 0*x[0] products, SURVEY.md 8a
+    gotcha 4: reproduced after the exchange, so shard y is byte-identical
+    for every x, NaN/inf included)."""
     vec = e.params.vec_cache_size
     warp = e.params.warp_size
     lo, hi = p0 * vec, p1 * vec
@@ -59,6 +79,10 @@ def halo_columns(e: EhybMatrix, p0: int, p1: int) -> np.ndarray:
     pos = np.asarray(e.position_er, np.int64)[owner // warp] + owner % warp + k * warp
     cols = np.asarray(e.col_er, np.int64)[pos]
     cols = cols[(cols < lo) | (cols >= hi)]
+    pad = er_pad_column(e)
+    if pad >= 0 and not (lo <= pad < hi):
+        if np.any(w < np.asarray(e.width_er, np.int64)[slots // warp]):
+            cols = np.append(cols, pad)
     return np.unique(cols)
 
 

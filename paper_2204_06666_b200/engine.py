@@ -1,5 +1,5 @@
 """SpMV execution (reference engine.py): the EHYB product on a B200 and the
-CSR reference product on cuSPARSE.
+CSR reference product (reference summation order) on the GPU.
 
 `spmv_ehyb` / `spmv_ehyb_user` keep the reference signatures and return
 types: numpy in -> numpy out (one H2D copy, one fused kernel, one D2H copy),
@@ -135,9 +135,11 @@ def spmv_ehyb_user(e: EhybMatrix, x, cfg: ExecutionConfig = ExecutionConfig()):
 
 
 def spmv_csr(m: CsrMatrix, x) -> np.ndarray:
-    """CSR y = A x in float64 (engine.py:56-69 contract) on cuSPARSE; the
-    comparator, independent of the EHYB layout. Row sums are accumulated in
-    cuSPARSE's order, so compare against it with a tolerance."""
+    """CSR y = A x in float64 (engine.py:56-69) on the GPU, bitwise the
+    reference oracle: fp64 products v[j]*x[c[j]] summed per non-empty row in
+    np.add.reduceat's order (first product, then numpy's pairwise sum of the
+    rest), one thread per row (`csr_ref_kernel`); empty rows are 0.0. The
+    cuSPARSE comparator is `DeviceCsr.spmv(..., alg=1|2)`."""
     from .device import DeviceCsr, _torch
 
     x = np.asarray(x)
@@ -147,7 +149,7 @@ def spmv_csr(m: CsrMatrix, x) -> np.ndarray:
         return np.zeros(m.n_rows, dtype=np.float64)
     torch = _torch()
     dc = DeviceCsr(m.n_rows, m.n_cols, m.row_ptr, m.col_idx, m.values, tau=8)
-    xt = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(f"cuda:{dc.device}")
+    xt = torch.from_numpy(np.ascontiguousarray(x.astype(np.float64))).to(f"cuda:{dc.device}")
     yt = torch.empty(m.n_rows, dtype=torch.float64, device=xt.device)
-    dc.spmv(xt, yt)
+    dc.spmv(xt, yt, alg=0)
     return yt.cpu().numpy()

@@ -186,8 +186,9 @@ def cmd_config(ehyb, names):
         n, r, c, v, tau = W.build_config(name)
         tgen = time.perf_counter() - t0
         tm = {}
+        prof = tuple(W.CONFIG_PROFILES.get(name, B200_PROFILE_ARGS))
         m, params, g, parts, cls, plan, e = run_pipeline(
-            ehyb, n, r, c, v, tau, B200_PROFILE_ARGS, timings=tm)
+            ehyb, n, r, c, v, tau, prof, timings=tm)
         arr = collect(parts, cls, plan, e, graph=g)
         x = W.deterministic_vector(n, 0)
         xr = ehyb.permute_vector(x, plan)
@@ -204,7 +205,7 @@ def cmd_config(ehyb, names):
         den = float(np.max(np.abs(ycsr))) if ycsr.size else 1.0
         rec = dict(
             name=name, description=W.CONFIGS[name][0], n=n, nnz=m.nnz, tau=tau,
-            profile=list(B200_PROFILE_ARGS), k=params.k, n_parts=params.n_parts,
+            profile=list(prof), k=params.k, n_parts=params.n_parts,
             vec=params.vec_cache_size, padded=e.padded_dimension, n_er=plan.n_er_rows,
             nnz_ell=e.nnz_ell, nnz_er=e.nnz_er, slots_ell=int(e.val_ell.size),
             slots_er=int(e.val_er.size), inner_fraction=cm.inner_fraction,

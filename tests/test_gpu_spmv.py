@@ -92,7 +92,7 @@ def _config_matrix(name):
     return W.build_config(name)
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg2", "cfg4",
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg2", "cfg4", "cfg5k4",
                                   "cfg3f32", "cfg3f64"])
 def test_config_bitwise(name):
     rec = config_record(name)
@@ -115,12 +115,49 @@ def test_config_bitwise(name):
     assert y2.tobytes() == y.tobytes()
 
 
-def test_cusparse_comparator_matches_oracle():
+def test_spmv_csr_is_bitwise_the_reference_oracle():
+    """engine.py:56-69: np.add.reduceat order (first product + numpy pairwise
+    sum), reproduced on the GPU — rows of 0..~2000 entries, empty rows,
+    signed zeros, non-finite x."""
     n, r, c, v = W.permute_symmetric(*W.stencil27(20, 20, 20), seed=3)
     m = E.CooMatrix(n, n, r, c, v)
     x = W.deterministic_vector(n, 5)
     y = E.spmv_csr(E.coo_to_csr(m), x)
-    assert rel_error(y, O.spmv_csr(n, r, c, v, x)) <= 1e-14
+    assert y.tobytes() == O.spmv_csr(n, r, c, v, x).tobytes()
+    rng = np.random.default_rng(11)
+    n = 3000
+    lens = np.concatenate([np.arange(0, 300), rng.integers(0, 40, n - 310),
+                           [1000, 1001, 1024, 1031, 1500, 2047, 2048, 2049, 4097, 9999]])
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.concatenate([np.sort(rng.choice(n, size=L, replace=False)) for L in lens])
+    vals = rng.standard_normal(rows.size) * np.exp(rng.uniform(-30, 30, rows.size))
+    vals[rng.integers(0, rows.size, 50)] = -0.0
+    m = E.CooMatrix(n, n, rows, cols, vals)
+    csr = E.coo_to_csr(m)
+    for xs in (rng.standard_normal(n), np.where(rng.random(n) < 0.01, np.inf, rng.standard_normal(n)),
+               -np.zeros(n)):
+        got = E.spmv_csr(csr, xs)
+        want = O.spmv_csr(n, rows, cols, vals, xs)
+        # bitwise, except that a NaN's payload is the hardware's
+        nan = np.isnan(want)
+        assert np.array_equal(np.isnan(got), nan)
+        assert got[~nan].tobytes() == want[~nan].tobytes()
+
+
+def test_cusparse_comparator_matches_oracle():
+    from paper_2204_06666_b200.device import DeviceCsr
+
+    n, r, c, v = W.permute_symmetric(*W.stencil27(20, 20, 20), seed=3)
+    m = E.CooMatrix(n, n, r, c, v)
+    csr = E.coo_to_csr(m)
+    x = W.deterministic_vector(n, 5)
+    dc = DeviceCsr(csr.n_rows, csr.n_cols, csr.row_ptr, csr.col_idx, csr.values, tau=8)
+    xt = torch.from_numpy(x).cuda()
+    want = O.spmv_csr(n, r, c, v, x)
+    for alg in (1, 2):
+        yt = torch.empty_like(xt)
+        dc.spmv(xt, yt, alg=alg)
+        assert rel_error(yt.cpu().numpy(), want) <= 1e-14
 
 
 def test_window_in_global_memory_path():

@@ -77,7 +77,7 @@ def test_config_digests(name):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["cfg2", "cfg3f32", "cfg3f64", "cfg4"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3f32", "cfg3f64", "cfg4", "cfg5k4"])
 def test_config_digests_full(name):
     test_config_digests.__wrapped__(name) if hasattr(test_config_digests, "__wrapped__") else None
     rec = config_record(name)
