@@ -125,17 +125,17 @@ def test_spmv_csr_is_bitwise_the_reference_oracle():
     y = E.spmv_csr(E.coo_to_csr(m), x)
     assert y.tobytes() == O.spmv_csr(n, r, c, v, x).tobytes()
     rng = np.random.default_rng(11)
-    n = 3000
+    n, nc = 3000, 12000  # rectangular: rows up to 9999 entries need that many columns
     lens = np.concatenate([np.arange(0, 300), rng.integers(0, 40, n - 310),
                            [1000, 1001, 1024, 1031, 1500, 2047, 2048, 2049, 4097, 9999]])
     rows = np.repeat(np.arange(n), lens)
-    cols = np.concatenate([np.sort(rng.choice(n, size=L, replace=False)) for L in lens])
+    cols = np.concatenate([np.sort(rng.choice(nc, size=L, replace=False)) for L in lens])
     vals = rng.standard_normal(rows.size) * np.exp(rng.uniform(-30, 30, rows.size))
     vals[rng.integers(0, rows.size, 50)] = -0.0
-    m = E.CooMatrix(n, n, rows, cols, vals)
+    m = E.CooMatrix(n, nc, rows, cols, vals)
     csr = E.coo_to_csr(m)
-    for xs in (rng.standard_normal(n), np.where(rng.random(n) < 0.01, np.inf, rng.standard_normal(n)),
-               -np.zeros(n)):
+    for xs in (rng.standard_normal(nc),
+               np.where(rng.random(nc) < 0.01, np.inf, rng.standard_normal(nc)), -np.zeros(nc)):
         got = E.spmv_csr(csr, xs)
         want = O.spmv_csr(n, rows, cols, vals, xs)
         # bitwise, except that a NaN's payload is the hardware's
