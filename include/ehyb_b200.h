@@ -50,6 +50,10 @@ extern "C" {
 /* SpMV arithmetic modes */
 #define EHYB_MODE_STRICT 0 /* separately rounded mul + add, k ascending: bitwise == reference */
 #define EHYB_MODE_FMA 1    /* fused multiply-add; within 1e-12 (fp64) / 1e-5 (fp32) */
+#define EHYB_MODE_DEFAULT 2 /* STRICT for every slice row; rows wider than the long-row
+                               threshold (EHYB_LONG_ROW, 128 entries) are summed in fixed
+                               4096-entry segments (deterministic, reassociated: within
+                               1e-12 (fp64) / 1e-5 (fp32)). == STRICT when no row is long */
 
 /* ------------------------------------------------------------ utilities */
 EHYB_API const char* ehyb_last_error(void);
@@ -191,6 +195,8 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
 #define EHYB_TUNE_TIMING 4
 #define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 4) */
 #define EHYB_TUNE_CLAIM_AHEAD 6 /* bit0: ELL chunks, bit1: ER slices claimed one ahead */
+#define EHYB_TUNE_PHASES 7      /* measurement only: bit0 skips the ER work, bit1 the ELL
+                                   stream (y is then incomplete) */
 EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value);
 
 /* spmv_ehyb (engine.py:108-216) in reordered space: y[padded] = A x[padded].

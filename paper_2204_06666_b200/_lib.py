@@ -18,9 +18,19 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libehyb_b200.so")
 
 EINVAL, ENOMEM, ECUDA = 1, 2, 3
-MODE_STRICT, MODE_FMA = 0, 1
+MODE_STRICT, MODE_FMA, MODE_DEFAULT = 0, 1, 2
+
+
+def mode(fma: bool = False, exact: bool = False) -> int:
+    """include/ehyb_b200.h EHYB_MODE_*: fma -> FMA; exact -> STRICT (every row
+    bitwise, long rows as one serial chain); else DEFAULT (bitwise except
+    rows wider than the long-row threshold, summed in fixed segments)."""
+    if fma:
+        return MODE_FMA
+    return MODE_STRICT if exact else MODE_DEFAULT
 TUNE_PREFETCH_ELL, TUNE_PREFETCH_ER, TUNE_THREADS, TUNE_TIMING, TUNE_ER_WARPS = 1, 2, 3, 4, 5
 TUNE_CLAIM_AHEAD = 6
+TUNE_PHASES = 7
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

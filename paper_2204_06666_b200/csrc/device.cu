@@ -146,6 +146,7 @@ struct ehyb_dev {
   int32_t* st_chunks = nullptr;
   uint2* ch_stage = nullptr;
   int ell_ahead = 1, er_ahead = 1;
+  int phase_skip = 0;  // EHYB_TUNE_PHASES (dev): bit 0 skips the ER work, bit 1 the ELL stream
   // ER padding column (SURVEY.md 8a gotcha 4): x index of the column the
   // reference's padding slots hold; shards without it locally fix up later
   int64_t er_pad_idx = 0;
@@ -198,7 +199,7 @@ struct ehyb_dev {
 
 namespace {
 
-template <typename T, bool STRICT, bool C32>
+template <typename T, int MODE, bool C32>
 cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell, bool do_er,
                          cudaStream_t st) {
   SpmvParams<T> P;
@@ -212,7 +213,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   // are all owned, pool included), halo phase (ER rows with a halo column and
   // long rows, after the exchange)
   P.er_sel = (do_ell && do_er) ? 0 : (do_ell ? 1 : 2);
-  do_er = true;
+  do_er = !(h->phase_skip & 1);  // dev measurement: EHYB_TUNE_PHASES bit 0 = no ER work
   P.er_pos = h->er_pos;
   P.er_swidth = h->er_swidth;
   P.er_rows = h->er_rows;
@@ -226,7 +227,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.warp = int32_t(h->warp);
   P.window_in_smem = (do_ell && h->window_in_smem) ? 1 : 0;
   P.window_tma = h->window_tma ? 1 : 0;
-  P.do_ell = do_ell ? 1 : 0;
+  P.do_ell = (do_ell && !(h->phase_skip & 2)) ? 1 : 0;
   P.do_er = do_er ? 1 : 0;
   P.pf_ell = h->pf_ell;
   P.pf_er = h->pf_er;
@@ -284,8 +285,8 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
     P.pool_last_scratch = 0;
   }
   void (*kern)(const SpmvParams<T>) = (do_ell && h->window_in_smem)
-                                           ? spmv_fused_kernel<T, STRICT, C32, true, false>
-                                           : spmv_fused_kernel<T, STRICT, C32, false, false>;
+                                           ? spmv_fused_kernel<T, MODE, C32, true, false>
+                                           : spmv_fused_kernel<T, MODE, C32, false, false>;
   // dynamic smem: [window | own-ER buffer | ELL ring]; the buffer is only
   // used when one launch runs both phases, the ring by any ELL launch
   size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
@@ -295,7 +296,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.ch_stage = nullptr;
   if constexpr (C32) {
     if (do_ell && h->window_in_smem && h->window_tma && h->ring_bytes > 0 && h->threads >= 64) {
-      kern = spmv_fused_kernel<T, STRICT, true, true, true>;
+      kern = spmv_fused_kernel<T, MODE, true, true, true>;
       P.ring_offset = int32_t(h->ring_offset);
       P.ring_stages = h->ring_stages;
       P.stage_bytes = h->stage_bytes;
@@ -309,7 +310,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
     }
   }
   if constexpr (C32) {
-    if (h->p2p_active) kern = spmv_fused_kernel<T, STRICT, true, true, false, true>;
+    if (h->p2p_active) kern = spmv_fused_kernel<T, MODE, true, true, false, true>;
   }
   if (!(do_ell && do_er)) {
     P.er_buf_slices = 0;
@@ -355,14 +356,19 @@ cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, boo
                         cudaStream_t st) {
   const bool c32 = h->warp == 32;
   if (mode == EHYB_MODE_FMA)
-    return c32 ? launch_typed<T, false, true>(h, x, y, ell, er, st)
-               : launch_typed<T, false, false>(h, x, y, ell, er, st);
-  return c32 ? launch_typed<T, true, true>(h, x, y, ell, er, st)
-             : launch_typed<T, true, false>(h, x, y, ell, er, st);
+    return c32 ? launch_typed<T, EHYB_MODE_FMA, true>(h, x, y, ell, er, st)
+               : launch_typed<T, EHYB_MODE_FMA, false>(h, x, y, ell, er, st);
+  if (mode == EHYB_MODE_DEFAULT)
+    return c32 ? launch_typed<T, EHYB_MODE_DEFAULT, true>(h, x, y, ell, er, st)
+               : launch_typed<T, EHYB_MODE_DEFAULT, false>(h, x, y, ell, er, st);
+  return c32 ? launch_typed<T, EHYB_MODE_STRICT, true>(h, x, y, ell, er, st)
+             : launch_typed<T, EHYB_MODE_STRICT, false>(h, x, y, ell, er, st);
 }
 
 cudaError_t launch_spmv(ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
                         cudaStream_t st) {
+  if (mode != EHYB_MODE_STRICT && mode != EHYB_MODE_FMA && mode != EHYB_MODE_DEFAULT)
+    return cudaErrorInvalidValue;
   cudaError_t e = h->tau == 4 ? launch_mode<float>(h, x, y, mode, ell, er, st)
                               : launch_mode<double>(h, x, y, mode, ell, er, st);
   if (e != cudaSuccess || !er || h->padfix_n == 0) return e;
@@ -385,26 +391,28 @@ double env_double(const char* name, double dflt) {
   return std::atof(v);
 }
 
-template <typename T, bool STRICT>
+template <typename T, int MODE>
 const void* fused_variant(bool c32, bool smem) {
-  return c32 ? (smem ? (const void*)spmv_fused_kernel<T, STRICT, true, true, false>
-                     : (const void*)spmv_fused_kernel<T, STRICT, true, false, false>)
-             : (smem ? (const void*)spmv_fused_kernel<T, STRICT, false, true, false>
-                     : (const void*)spmv_fused_kernel<T, STRICT, false, false, false>);
+  return c32 ? (smem ? (const void*)spmv_fused_kernel<T, MODE, true, true, false>
+                     : (const void*)spmv_fused_kernel<T, MODE, true, false, false>)
+             : (smem ? (const void*)spmv_fused_kernel<T, MODE, false, true, false>
+                     : (const void*)spmv_fused_kernel<T, MODE, false, false, false>);
 }
 
 // resident CTAs per SM of the fused kernel for this handle's configuration:
-// the minimum over the strict and FMA variants, so every launch mode fits
+// the minimum over the arithmetic-mode variants, so every launch mode fits
 // the one grid the persistent-group layout was built for
 cudaError_t occupancy(const ehyb_dev* h, int* per_sm) {
   const bool c32 = h->warp == 32;
-  const void* ks[2];
+  const void* ks[3];
   if (h->tau == 4) {
-    ks[0] = fused_variant<float, true>(c32, h->window_in_smem);
-    ks[1] = fused_variant<float, false>(c32, h->window_in_smem);
+    ks[0] = fused_variant<float, EHYB_MODE_STRICT>(c32, h->window_in_smem);
+    ks[1] = fused_variant<float, EHYB_MODE_FMA>(c32, h->window_in_smem);
+    ks[2] = fused_variant<float, EHYB_MODE_DEFAULT>(c32, h->window_in_smem);
   } else {
-    ks[0] = fused_variant<double, true>(c32, h->window_in_smem);
-    ks[1] = fused_variant<double, false>(c32, h->window_in_smem);
+    ks[0] = fused_variant<double, EHYB_MODE_STRICT>(c32, h->window_in_smem);
+    ks[1] = fused_variant<double, EHYB_MODE_FMA>(c32, h->window_in_smem);
+    ks[2] = fused_variant<double, EHYB_MODE_DEFAULT>(c32, h->window_in_smem);
   }
   *per_sm = 1 << 30;
   for (const void* k : ks) {
@@ -595,9 +603,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->win_bytes = h->window_in_smem ? win_al : 0;
   h->window_tma = h->window_in_smem && (win % 16 == 0);  // TMA needs 16 B multiples
   h->er_buf_offset = int(h->win_bytes);
+  const size_t buf_slot = size_t(tb);  // own-ER buffer: one sum per buffered row
   h->er_buf_slices = int(std::min<size_t>(
-      kMaxErBuf, (size_t(optin) - h->win_bytes - kStaticReserve) / (32 * tb)));
-  h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
+      kMaxErBuf, (size_t(optin) - h->win_bytes - kStaticReserve) / (32 * buf_slot)));
+  h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * buf_slot;
   const int64_t chunks = (vec + 31) / 32;
   // one warp per chunk up to 1024 threads, plus the ring producer warp
   h->threads = int(std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, chunks * 32 + 32)));
@@ -695,7 +704,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     // (large windows, e.g. cfg5) spill the rest to a global scratch, so the
     // ER-first warps still finish them during the ELL phase
     own_scratch = max_own > h->er_buf_slices && env_double("EHYB_OWN_SCRATCH", 0.0) != 0.0;
-    h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * tb;
+    h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * buf_slot;
     // ELL ring (C == 32, TMA-staged window): shared memory left after the
     // window, at least 2 chunks of the widest slice; the own-ER buffer gives
     // way so the ring keeps >= EHYB_RING_KB (default 64 KB)
@@ -703,18 +712,18 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     if (C == 32 && h->window_tma && env_double("EHYB_RING", 0.0) != 0.0) {
       cudaFuncAttributes fa{};
       if (tb == 4)
-        CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<float, true, true, true, true>));
+        CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<float, EHYB_MODE_STRICT, true, true, true>));
       else
-        CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<double, true, true, true, true>));
+        CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<double, EHYB_MODE_STRICT, true, true, true>));
       const int64_t dyn = int64_t(optin) - int64_t(fa.sharedSizeBytes) - 256;
       const int64_t avail = dyn - int64_t(h->win_bytes);
       const int64_t want = std::max<int64_t>(2 * max_chunk_bytes,
                                              int64_t(env_double("EHYB_RING_KB", 64.0) * 1024.0));
       if (avail >= 2 * max_chunk_bytes && avail >= 16 * 1024) {
-        int64_t buf = int64_t(h->er_buf_slices) * 32 * int64_t(tb);
+        int64_t buf = int64_t(h->er_buf_slices) * 32 * int64_t(buf_slot);
         if (avail - buf < want) buf = std::max<int64_t>(0, avail - want);
-        h->er_buf_slices = int(buf / (32 * int64_t(tb)));
-        buf = int64_t(h->er_buf_slices) * 32 * int64_t(tb);
+        h->er_buf_slices = int(buf / (32 * int64_t(buf_slot)));
+        buf = int64_t(h->er_buf_slices) * 32 * int64_t(buf_slot);
         h->ring_offset = (size_t(h->win_bytes) + size_t(buf) + 127) / 128 * 128;
         const int64_t total = (dyn - int64_t(h->ring_offset)) / 128 * 128;
         // stages of ~EHYB_STAGE_KB (default 16 KB), 2..kRingNS-1 of them; each
@@ -1039,6 +1048,7 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
       h->ell_ahead = int(value & 1);
       h->er_ahead = int((value >> 1) & 1);
       return 0;
+    case EHYB_TUNE_PHASES: h->phase_skip = int(value & 3); return 0;
     case EHYB_TUNE_TIMING:
       h->timing = reinterpret_cast<unsigned long long*>(static_cast<uintptr_t>(value));
       return 0;

@@ -379,9 +379,15 @@ constexpr int kRingFB = 64;  // full barriers, by stage number mod 64: a consume
 // instruction — then the W % 4 tail in SELL order. UB blocks per batch keep
 // the same bytes in flight as the scalar path with fewer registers and a
 // quarter of the load instructions. Accumulation is k ascending.
+#ifndef EHYB_VEC_UB_F32
+#define EHYB_VEC_UB_F32 4
+#endif
+#ifndef EHYB_VEC_UB_F64
+#define EHYB_VEC_UB_F64 2
+#endif
 template <typename T>
 struct VecBlocks {
-  static constexpr int value = sizeof(T) == 4 ? 4 : 2;
+  static constexpr int value = sizeof(T) == 4 ? EHYB_VEC_UB_F32 : EHYB_VEC_UB_F64;
 };
 
 template <typename T>
@@ -412,33 +418,11 @@ __device__ __forceinline__ T ell_slice32_vec(const T* __restrict__ val,
   constexpr int UB = VecBlocks<T>::value;
   T acc = T(0);
   const int nb = w >> 2;
+  const int nt = w & 3;
   const T* vb = val + pos + 4 * lane;
   const uint16_t* cb = col + pos + 4 * lane;
   bool waited = false;
-  for (int b = 0; b < nb; b += UB) {
-    T v[4 * UB];
-    uint2 c[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      c[u] = make_uint2(0u, 0u);
-      if (b + u < nb) c[u] = __ldcs(reinterpret_cast<const uint2*>(cb + 128 * (b + u)));
-    }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      if (b + u < nb) {
-        ld_block4<T>(vb + 128 * (b + u), v + 4 * u);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[4 * u + j] = T(0);
-      }
-    }
-    if constexpr (WAIT) {
-      if (!waited) {
-        mbar_wait(win_bar, win_phase);
-        waited = true;
-      }
-    }
-    T xv[4 * UB];
+  auto gather_blocks = [&](const uint2* c, T* xv) {
 #pragma unroll
     for (int u = 0; u < UB; ++u) {
       xv[4 * u + 0] = win[c[u].x & 0xffffu];
@@ -446,21 +430,77 @@ __device__ __forceinline__ T ell_slice32_vec(const T* __restrict__ val,
       xv[4 * u + 2] = win[c[u].y & 0xffffu];
       xv[4 * u + 3] = win[c[u].y >> 16];
     }
+  };
+  int b = 0;
+  // full batches: UB blocks each, while more than UB blocks remain
+  for (; b + UB < nb; b += UB) {
+    T v[4 * UB];
+    uint2 c[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) c[u] = __ldcs(reinterpret_cast<const uint2*>(cb + 128 * (b + u)));
+#pragma unroll
+    for (int u = 0; u < UB; ++u) ld_block4<T>(vb + 128 * (b + u), v + 4 * u);
+    if constexpr (WAIT) {
+      if (!waited) {
+        mbar_wait(win_bar, win_phase);
+        waited = true;
+      }
+    }
+    T xv[4 * UB];
+    gather_blocks(c, xv);
+#pragma unroll
+    for (int j = 0; j < 4 * UB; ++j) acc = madd<STRICT>(acc, v[j], xv[j]);
+  }
+  // last batch: the remaining (<= UB) blocks AND the W % 4 tail (SELL order
+  // after the blocks) issued together, so a narrow slice costs one round trip
+  {
+    const int rb = nb - b;
+    T v[4 * UB];
+    uint2 c[UB];
+    T tv[3];
+    uint32_t tc[3];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      c[u] = make_uint2(0u, 0u);
+      if (u < rb) c[u] = __ldcs(reinterpret_cast<const uint2*>(cb + 128 * (b + u)));
+    }
+    const int64_t tpos = pos + 128 * int64_t(nb) + lane;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      tc[j] = 0;
+      if (j < nt) tc[j] = __ldcs(col + tpos + 32 * j);
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      if (u < rb) {
+        ld_block4<T>(vb + 128 * (b + u), v + 4 * u);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[4 * u + j] = T(0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      tv[j] = T(0);
+      if (j < nt) tv[j] = __ldcs(val + tpos + 32 * j);
+    }
+    if constexpr (WAIT) {
+      if (!waited) mbar_wait(win_bar, win_phase);
+    }
+    T xv[4 * UB];
+    gather_blocks(c, xv);
+    T tx[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) tx[j] = win[tc[j]];
 #pragma unroll
     for (int u = 0; u < UB; ++u)
-      if (b + u < nb) {
+      if (u < rb) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc = madd<STRICT>(acc, v[4 * u + j], xv[4 * u + j]);
       }
-  }
-  if constexpr (WAIT) {
-    if (!waited) mbar_wait(win_bar, win_phase);
-  }
-  // W % 4 tail, SELL order after the blocks
-  const int64_t tpos = pos + 128 * int64_t(nb) + lane;
-  for (int k = 4 * nb; k < w; ++k) {
-    const int64_t i = tpos + 32 * int64_t(k - 4 * nb);
-    acc = madd<STRICT>(acc, __ldcs(val + i), win[__ldcs(col + i)]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (j < nt) acc = madd<STRICT>(acc, tv[j], tx[j]);
   }
   return acc;
 }
@@ -710,16 +750,18 @@ __device__ __forceinline__ T long_finish(const SpmvParams<T>& P, int task, T ell
 // Long-row work of one warp, claimed from a grid-wide counter: whole rows in
 // STRICT mode (serial chains, longest first), segments in FMA mode (the last
 // segment of a row to finish sums the partials in segment order).
-template <typename T, bool STRICT>
+template <typename T, int MODE>
 __device__ void long_rows_warp(const SpmvParams<T>& P, int lane, T* stage, uint32_t ep) {
   unsigned int* ctr = P.lr_ctr + (ep & 1u);
-  const int n_items = STRICT ? P.lr_tasks : P.lr_segs;
+  // EHYB_MODE_STRICT: one serial chain per row; DEFAULT / FMA: segments
+  constexpr bool serial = MODE == EHYB_MODE_STRICT;
+  const int n_items = serial ? P.lr_tasks : P.lr_segs;
   for (;;) {
     unsigned int v = 0;
     if (lane == 0) v = atomicAdd(ctr, 1u);
     const int item = int(__shfl_sync(0xffffffffu, v, 0));
     if (item >= n_items) break;
-    if constexpr (STRICT) {
+    if constexpr (serial) {
       const int64_t lo = __ldg(P.lr_span + 3 * item), mid = __ldg(P.lr_span + 3 * item + 1),
                     hi = __ldg(P.lr_span + 3 * item + 2);
       const T ell = long_chain_strict(P, lo, mid, lane, stage);
@@ -970,8 +1012,11 @@ constexpr int kMaxErBuf = 2048;                        // buffered own ER slices
 // warp moves straight on to the partition's ER slices (no CTA barrier). An
 // ER row whose ELL chunk is still in flight waits on that chunk's done bit,
 // so y[r] = y_ell[r] + er_acc keeps the reference's order of operations.
-template <typename T, bool STRICT, bool C32, bool SMEM, bool RING, bool P2P = false>
+template <typename T, int MODE, bool C32, bool SMEM, bool RING, bool P2P = false>
 __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvParams<T> P) {
+  // EHYB_MODE_*: STRICT and DEFAULT round every slice product and add
+  // separately (reference order); they differ only in the long-row path
+  constexpr bool STRICT = MODE != EHYB_MODE_FMA;
   static_assert(!RING || (C32 && SMEM), "the ELL ring needs 32-row slices and a staged window");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar;
@@ -1129,7 +1174,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   // longest dependent work of the launch
   if (it == 0 && P.do_er && P.lr_tasks > 0 && wid == 0) {
     wait_halo();
-    long_rows_warp<T, STRICT>(P, lane, lr_stage, ep);
+    long_rows_warp<T, MODE>(P, lane, lr_stage, ep);
   }
 
   // own ER slices [s0, s1): the first n_buf are computed into a buffer at

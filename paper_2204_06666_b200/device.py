@@ -69,7 +69,7 @@ class DeviceMatrix:
 
     def tune(self, *, prefetch_ell: int | None = None, prefetch_er: bool | None = None,
              threads: int | None = None, timing=False, er_warps: int | None = None,
-             claim_ahead: int | None = None) -> None:
+             claim_ahead: int | None = None, phases: int | None = None) -> None:
         """Launch knobs (include/ehyb_b200.h ehyb_dev_tune). `timing`: a CUDA
         int64 tensor of n_ctas*8 zeroed entries to record per-CTA stamps, None to
         stop recording, False (default) to leave it unchanged."""
@@ -83,6 +83,8 @@ class DeviceMatrix:
             L.call("ehyb_dev_tune", self._h, L.TUNE_ER_WARPS, int(er_warps))
         if claim_ahead is not None:
             L.call("ehyb_dev_tune", self._h, L.TUNE_CLAIM_AHEAD, int(claim_ahead))
+        if phases is not None:  # measurement only: 1 = ELL alone, 2 = ER alone, 0 = both
+            L.call("ehyb_dev_tune", self._h, L.TUNE_PHASES, int(phases))
         if timing is not False:
             ptr = 0 if timing is None else int(timing.data_ptr())
             L.call("ehyb_dev_tune", self._h, L.TUNE_TIMING, ptr)
@@ -110,8 +112,12 @@ class DeviceMatrix:
         if t.device.index != self.device:
             raise ValueError(f"{what} lives on cuda:{t.device.index}, matrix on cuda:{self.device}")
 
-    def spmv(self, x, y=None, *, fma: bool = False, stream=None):
-        """y = A x in reordered space, device tensors, stream-ordered."""
+    def spmv(self, x, y=None, *, fma: bool = False, exact: bool = False, stream=None):
+        """y = A x in reordered space, device tensors, stream-ordered.
+        Arithmetic (include/ehyb_b200.h EHYB_MODE_*): default = the reference's
+        rounding for every slice row (bitwise), rows wider than the long-row
+        threshold summed in fixed segments (1e-12 / 1e-5); exact=True = every
+        row bitwise (long rows as one serial chain); fma=True = fused."""
         torch = _torch()
         self._check_tensor(x, self.padded, "x")
         if y is None:
@@ -119,10 +125,10 @@ class DeviceMatrix:
         else:
             self._check_tensor(y, self.padded, "y")
         L.call("ehyb_dev_spmv", self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
-               L.MODE_FMA if fma else L.MODE_STRICT, _stream_ptr(stream, self.device))
+               L.mode(fma, exact), _stream_ptr(stream, self.device))
         return y
 
-    def spmv_user(self, x, y=None, *, fma: bool = False, stream=None):
+    def spmv_user(self, x, y=None, *, fma: bool = False, exact: bool = False, stream=None):
         """Original-order y = A x on device tensors (permute, spmv, unpermute)."""
         torch = _torch()
         self._check_tensor(x, self.dimension, "x")
@@ -131,7 +137,7 @@ class DeviceMatrix:
         else:
             self._check_tensor(y, self.dimension, "y")
         L.call("ehyb_dev_spmv_user", self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
-               L.MODE_FMA if fma else L.MODE_STRICT, _stream_ptr(stream, self.device))
+               L.mode(fma, exact), _stream_ptr(stream, self.device))
         return y
 
     def permute(self, x, out=None, stream=None):
@@ -153,7 +159,7 @@ class DeviceMatrix:
         return out
 
     def spmv_host(self, x: np.ndarray, *, user_order: bool, fma: bool = False,
-                  out: np.ndarray | None = None) -> np.ndarray:
+                  exact: bool = False, out: np.ndarray | None = None) -> np.ndarray:
         """Host arrays in, host array out: H2D copy, fused kernel, D2H copy,
         synchronised (the path a numpy caller of the reference API takes)."""
         length = self.dimension if user_order else self.padded
@@ -163,11 +169,12 @@ class DeviceMatrix:
                              + ("the matrix dimension" if user_order else "padded_dimension entries"))
         y = np.empty(length, dtype=self.dtype) if out is None else out
         L.call("ehyb_dev_spmv_host", self._h, C.c_void_p(x.ctypes.data), C.c_void_p(y.ctypes.data),
-               1 if user_order else 0, L.MODE_FMA if fma else L.MODE_STRICT,
+               1 if user_order else 0, L.mode(fma, exact),
                _stream_ptr(None, self.device))
         return y
 
-    def spmv_host_many(self, xs, *, user_order: bool, fma: bool = False, out=None):
+    def spmv_host_many(self, xs, *, user_order: bool, fma: bool = False, exact: bool = False,
+                       out=None):
         """Independent products of several host vectors (ehyb_dev_spmv_host_many):
         each is copied in, multiplied and copied out like `spmv_host`, but the
         copy-in of the next vector and the copy-out of the previous one overlap
@@ -199,7 +206,7 @@ class DeviceMatrix:
         xp = (C.c_void_p * max(k, 1))(*[x.ctypes.data for x in xs])
         yp = (C.c_void_p * max(k, 1))(*[y.ctypes.data for y in ys])
         L.call("ehyb_dev_spmv_host_many", self._h, xp, yp, k, 1 if user_order else 0,
-               L.MODE_FMA if fma else L.MODE_STRICT, _stream_ptr(None, self.device))
+               L.mode(fma, exact), _stream_ptr(None, self.device))
         return out
 
 

@@ -412,23 +412,24 @@ class DistributedEhyb:
             return self._x_p2p
         return self.new_ext()
 
-    def spmv_local(self, x_ext, y_local, *, fma: bool = False):
+    def spmv_local(self, x_ext, y_local, *, fma: bool = False, exact: bool = False):
         """Both phases on an x_ext whose halo is already filled (no exchange)."""
         import torch
 
-        mode = L.MODE_FMA if fma else L.MODE_STRICT
+        mode = L.mode(fma, exact)
         st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         xp, yp = C.c_void_p(x_ext.data_ptr()), C.c_void_p(y_local.data_ptr())
         L.call("ehyb_dev_spmv_ell", self._h, xp, yp, mode, st)
         L.call("ehyb_dev_spmv_er", self._h, xp, yp, mode, st)
         return y_local
 
-    def spmv(self, x_ext, y_local, *, fma: bool = False, overlap: bool = True):
+    def spmv(self, x_ext, y_local, *, fma: bool = False, exact: bool = False,
+             overlap: bool = True):
         """y_local = A[owned rows, :] x. x_ext[:local_rows] holds the owned x;
         the halo part is exchanged here, overlapped with the ELL phase."""
         import torch
 
-        mode = L.MODE_FMA if fma else L.MODE_STRICT
+        mode = L.mode(fma, exact)
         st = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         if self._x_p2p is not None:
             # one fused launch: ELL, local ER, halo pull from peer memory, halo rows
@@ -452,7 +453,7 @@ class DistributedEhyb:
         return y_local
 
 
-    def spmv_host(self, x_local, y_local, *, fma: bool = False):
+    def spmv_host(self, x_local, y_local, *, fma: bool = False, exact: bool = False):
         """Host arrays in and out (pinned for the full PCIe rate): copy the
         owned x slice in, exchange the halo, multiply, copy the owned y out,
         synchronise — the end-to-end call of one rank."""
@@ -463,7 +464,7 @@ class DistributedEhyb:
             self._y_loc = torch.empty(self.local_rows, dtype=self.dtype,
                                       device=f"cuda:{self.device}")
         self._x_ext[: self.local_rows].copy_(torch.as_tensor(x_local), non_blocking=True)
-        self.spmv(self._x_ext, self._y_loc, fma=fma)
+        self.spmv(self._x_ext, self._y_loc, fma=fma, exact=exact)
         out = torch.as_tensor(y_local)
         out.copy_(self._y_loc, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()

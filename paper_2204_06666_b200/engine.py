@@ -24,14 +24,20 @@ SCHEDULING_MODES = ("static", "stealing")
 class ExecutionConfig:
     """Reference engine.py:27-40. worker_count / scheduling are validated and
     reported but do not change results (as in the reference); on the GPU the
-    schedule is one CTA per partition with in-CTA slice stealing. `fma`
-    (extension, default off) fuses multiply and add: faster to issue, within
-    1e-12 / 1e-5 instead of bitwise."""
+    schedule is one CTA per partition with in-CTA slice stealing. Extensions:
+    by default every row whose ELL/ER width is at most the long-row threshold
+    (128 entries) is computed with the reference's rounding (bitwise); wider
+    rows (heavy-tailed hubs) are summed in fixed 4096-entry segments, a
+    deterministic reassociation within 1e-12 (fp64) / 1e-5 (fp32) of the
+    serial sum. `exact=True` keeps those rows as one serial chain too (bitwise
+    everywhere, latency-bound on hub rows); `fma=True` fuses multiply and add
+    everywhere (within the same tolerances)."""
 
     worker_count: int = 1
     scheduling: str = "static"
     record_stats: bool = True
     fma: bool = False
+    exact: bool = False
 
     def __post_init__(self):
         if self.worker_count < 1:
@@ -107,12 +113,12 @@ def spmv_ehyb(e: EhybMatrix, x_reordered, cfg: ExecutionConfig = ExecutionConfig
         dm = device_matrix(e, x.device.index)
         if x.dtype != dm.torch_dtype:
             x = x.to(dm.torch_dtype)
-        y = dm.spmv(x.contiguous(), fma=cfg.fma)
+        y = dm.spmv(x.contiguous(), fma=cfg.fma, exact=cfg.exact)
         return y, exec_stats(e, cfg)
     x = np.asarray(x_reordered)
     if x.ndim != 1 or x.size != e.padded_dimension:
         raise ValueError("length mismatch: x must have padded_dimension entries")
-    y = device_matrix(e).spmv_host(x, user_order=False, fma=cfg.fma)
+    y = device_matrix(e).spmv_host(x, user_order=False, fma=cfg.fma, exact=cfg.exact)
     return y, exec_stats(e, cfg)
 
 
@@ -127,11 +133,11 @@ def spmv_ehyb_user(e: EhybMatrix, x, cfg: ExecutionConfig = ExecutionConfig()):
         dm = device_matrix(e, x.device.index)
         if x.dtype != dm.torch_dtype:
             x = x.to(dm.torch_dtype)
-        return dm.spmv_user(x.contiguous(), fma=cfg.fma)
+        return dm.spmv_user(x.contiguous(), fma=cfg.fma, exact=cfg.exact)
     x = np.asarray(x)
     if x.ndim != 1 or x.size != e.dimension:
         raise ValueError("length mismatch: vector does not match the plan dimension")
-    return device_matrix(e).spmv_host(x, user_order=True, fma=cfg.fma)
+    return device_matrix(e).spmv_host(x, user_order=True, fma=cfg.fma, exact=cfg.exact)
 
 
 def spmv_csr(m: CsrMatrix, x) -> np.ndarray:

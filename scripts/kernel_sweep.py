@@ -80,6 +80,7 @@ def main():
     ap.add_argument("--ring", default="0", help="EHYB_RING values (0 = register ELL path)")
     ap.add_argument("--stage-kb", default="16", help="EHYB_STAGE_KB values")
     ap.add_argument("--vec", default="0", help="EHYB_VEC values (0 = SELL layout, scalar loads)")
+    ap.add_argument("--phases", action="store_true", help="also time ELL alone and ER alone")
     args = ap.parse_args()
     m, e, _ = bench.build_workload(args.config)
     gold = bench.golden_y_digest(args.config)
@@ -120,6 +121,11 @@ def main():
                                 ring_kb=h.info()["ring_bytes"] // 1024, pf_ell=pfe, pf_er=pfer, er_warps=ew,
                                 ahead=ah, us=round(us, 2), gbs=round(bmin / us / 1e3, 1),
                                 bitwise=ok))
+            if args.phases:  # each phase alone (measurement-only launches)
+                for ph, key in ((1, "ell_only_us"), (2, "er_only_us")):
+                    h.tune(phases=ph)
+                    results[-1][key] = round(time_variant(h, xr, y, args.reps, stream), 2)
+                h.tune(phases=0)
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
     dm = handles[(best["pool"], best["er_cost"], best["ring"], best["stage_kb"], best["vec"])]
@@ -144,8 +150,11 @@ def main():
         ev1.synchronize()
         return round(ev0.elapsed_time(ev1) / args.reps * 1e3, 2)
 
-    prof["ell_only_us"] = phase_us("ehyb_dev_spmv_ell")
-    prof["er_only_us"] = phase_us("ehyb_dev_spmv_er")
+    dm.tune(phases=1)
+    prof["ell_only_us"] = round(time_variant(dm, xr, y, args.reps, stream), 2)
+    dm.tune(phases=2)
+    prof["er_only_us"] = round(time_variant(dm, xr, y, args.reps, stream), 2)
+    dm.tune(phases=0)
     us_fma = time_variant(dm, xr, y, args.reps, stream, fma=True)
     print(json.dumps({"config": args.config, "best": best, "cta_profile_best": prof,
                       "fma_us": round(us_fma, 2), "bmin": bmin}), flush=True)

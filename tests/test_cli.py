@@ -85,11 +85,11 @@ def test_bench_csv_schema_round_trip():
         nnz_ell=12, nnz_er=8, footprint_total_bytes=100, savings_vs_32bit_cols=0.1,
         traffic_model_bytes=200, workers=1, scheduling="static", reps=3, warmup=1,
         partition_s=0.1, reorder_assemble_s=0.2, prep_to_spmv_ratio=3.0,
-        kernels=[cli.KernelTiming("ehyb", 1e-5, 4.0), cli.KernelTiming("csr-cusparse", 2e-5, 2.0)])
+        kernels=[cli.KernelTiming("ehyb", 1e-5, 4.0), cli.KernelTiming("csr-oracle", 2e-5, 2.0)])
     buf = io.StringIO()
     cli.write_bench_csv(rep, buf)
     rows = cli.read_bench_csv(io.StringIO(buf.getvalue()))
-    assert [r["kernel"] for r in rows] == ["ehyb", "csr-cusparse"]
+    assert [r["kernel"] for r in rows] == ["ehyb", "csr-oracle"]
     assert rows[0]["schema_version"] == 1 and rows[0]["nnz"] == 20 and rows[1]["gflops"] == 2.0
     assert list(rows[0]) == cli.BENCH_CSV_COLUMNS
     with pytest.raises(ValueError, match="unsupported bench CSV schema"):
@@ -111,7 +111,8 @@ def test_verify_and_bench_on_gpu(tmp_path, capsys):
     assert json.loads(capsys.readouterr().out)["status"] == "pass"
     assert cli.main(["bench", str(path), "--reps", "5", "--warmup", "2", *flags]) == 0
     rep = json.loads(capsys.readouterr().out)
-    assert [k["kernel"] for k in rep["kernels"]] == ["ehyb", "csr-cusparse"]
+    assert [k["kernel"] for k in rep["kernels"]] == ["ehyb", "csr-oracle"]
+    assert rep["gpu"]["csr_cusparse"]["gflops"] > 0
     assert rep["gpu"]["effective_gbs"] > 0
     out = tmp_path / "b.csv"
     assert cli.main(["bench", str(path), "--reps", "3", "--out", "csv", "--output", str(out),

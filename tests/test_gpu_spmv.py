@@ -102,17 +102,28 @@ def test_config_bitwise(name):
     m, params, graph, parts, cls, plan, e = product_pipeline(n, r, c, v, tau, tuple(rec["profile"]))
     assert digest(e.val_ell) == rec["digests"]["val_ell"]
     x = W.deterministic_vector(n, 0)
-    y, _ = E.spmv_ehyb(e, E.permute_vector(x, plan))
+    exact = E.ExecutionConfig(exact=True)
+    y, _ = E.spmv_ehyb(e, E.permute_vector(x, plan), exact)
     assert digest(y) == rec["y_reordered"]
-    yu = E.spmv_ehyb_user(e, x)
+    yu = E.spmv_ehyb_user(e, x, exact)
     assert digest(yu) == rec["y_user"]
+    tol = 1e-12 if tau == 8 else 1e-5
     # FMA mode within the north-star tolerance of the strict result
     dm = E.device_matrix(e, 0)
     yt = dm.spmv_user(torch.from_numpy(x).to("cuda:0", dm.torch_dtype), fma=True)
-    assert rel_error(yt.cpu().numpy(), yu) <= (1e-12 if tau == 8 else 1e-5)
+    assert rel_error(yt.cpu().numpy(), yu) <= tol
+    # the default mode: bitwise unless the matrix has rows wider than the
+    # long-row threshold, whose segmented sums are within the tolerance
+    yd, _ = E.spmv_ehyb(e, E.permute_vector(x, plan))
+    if dm.info()["long_rows"] == 0:
+        assert yd.tobytes() == y.tobytes()
+    else:
+        assert rel_error(yd, y) <= tol
     # repeated launches are bit-identical (no atomics in the data path)
-    y2, _ = E.spmv_ehyb(e, E.permute_vector(x, plan))
+    y2, _ = E.spmv_ehyb(e, E.permute_vector(x, plan), exact)
     assert y2.tobytes() == y.tobytes()
+    yd2, _ = E.spmv_ehyb(e, E.permute_vector(x, plan))
+    assert yd2.tobytes() == yd.tobytes()
 
 
 def test_spmv_csr_is_bitwise_the_reference_oracle():
@@ -186,7 +197,7 @@ def test_non_finite_x_matches_reference_engine(tau):
         xb = xr.copy()
         xb[0] = bad
         xb[7] = -np.inf
-        y, _ = E.spmv_ehyb(e, xb)
+        y, _ = E.spmv_ehyb(e, xb, E.ExecutionConfig(exact=True))
         want = c_oracle.spmv_ehyb(e, xb)
         assert np.array_equal(np.isnan(y), np.isnan(want))
         fin = ~np.isnan(want)
@@ -278,20 +289,32 @@ def test_long_rows_bitwise_strict_and_fma_tolerance(monkeypatch, tau, case):
         want = c_oracle.spmv_ehyb(e, xr)
         xt = torch.from_numpy(xr).to("cuda:0", dt)
         for _ in range(3):  # repeated launches: per-launch counters reset
-            y = dm.spmv(xt)
+            y = dm.spmv(xt, exact=True)
             torch.cuda.synchronize()
             assert y.cpu().numpy().tobytes() == want.tobytes()
         yf = dm.spmv(xt, fma=True)
         yf2 = dm.spmv(xt, fma=True)
         torch.cuda.synchronize()
         assert yf.cpu().numpy().tobytes() == yf2.cpu().numpy().tobytes()  # deterministic
-        assert rel_error(yf.cpu().numpy(), want) <= (1e-12 if tau == 8 else 1e-5)
+        tol = 1e-12 if tau == 8 else 1e-5
+        assert rel_error(yf.cpu().numpy(), want) <= tol
+        # default mode: slice rows bitwise strict, long rows the segmented sums
+        # (the same code as FMA mode's long rows), deterministic
+        yd = dm.spmv(xt).cpu().numpy()
+        assert dm.spmv(xt).cpu().numpy().tobytes() == yd.tobytes()
+        assert rel_error(yd, want) <= tol
+        yfn = yf.cpu().numpy()
+        same = (yd.view(np.uint8).reshape(-1, yd.itemsize) == want.view(np.uint8).reshape(
+            -1, yd.itemsize)).all(1)
+        same |= (yd.view(np.uint8).reshape(-1, yd.itemsize) == yfn.view(np.uint8).reshape(
+            -1, yd.itemsize)).all(1)
+        assert same.all()
     # non-finite x: the reference's padding products propagate NaN/inf
     xb = E.permute_vector(W.deterministic_vector(n, 3), e.plan)
     xb[0] = np.nan
     xb[e.params.vec_cache_size] = np.inf
     want = c_oracle.spmv_ehyb(e, xb)
-    y = dm.spmv(torch.from_numpy(xb).to("cuda:0", dt)).cpu().numpy()
+    y = dm.spmv(torch.from_numpy(xb).to("cuda:0", dt), exact=True).cpu().numpy()
     assert np.array_equal(np.isnan(y), np.isnan(want))
     fin = ~np.isnan(want)
     assert y[fin].tobytes() == want[fin].tobytes()
@@ -359,3 +382,30 @@ def test_launch_kind_sequences_keep_per_launch_counters():
                        L.MODE_STRICT, st)
             torch.cuda.synchronize()
             assert y.cpu().numpy().tobytes() == want.tobytes(), seq
+
+
+def test_fused_launch_beside_busy_kernels():
+    # the fused kernel's pool / persistent-CTA protocols spin on flags other
+    # CTAs write; the cooperative launch keeps the whole grid co-resident
+    # while another stream keeps the SMs busy (GEMMs issued just before)
+    busy, work = torch.cuda.Stream(), torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda:0")
+    b = torch.randn(4096, 4096, device="cuda:0")
+    c = torch.empty_like(a)
+    for prof in (E.DeviceProfile(16, 32, 8192), E.DeviceProfile(600, 32, 4096)):
+        n, r, cc, v = W.permute_symmetric(*W.stencil27(24, 24, 24), seed=5)
+        e = E.build_ehyb(E.CooMatrix(n, n, r, cc, v), tau=8, profile=prof)
+        dm = E.device_matrix(e, 0)
+        xr = E.permute_vector(W.deterministic_vector(n, 9), e.plan)
+        want = c_oracle.spmv_ehyb(e, xr)
+        xt = torch.from_numpy(xr).to("cuda:0")
+        torch.cuda.synchronize()
+        ys = []
+        for _ in range(4):
+            with torch.cuda.stream(busy):
+                for _ in range(8):
+                    torch.mm(a, b, out=c)
+            ys.append(dm.spmv(xt, stream=work))
+        torch.cuda.synchronize()
+        for y in ys:
+            assert y.cpu().numpy().tobytes() == want.tobytes()
