@@ -508,7 +508,6 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       max_chunk_bytes = std::max<int64_t>(
           max_chunk_bytes, (int64_t(e & kEffWidth) * int64_t(C) * int64_t(tb + 2) + 127) / 128 * 128);
     }
-    CUDA_TRY(upload(&h->width_ell, eff.data(), eff.size() * 4, &h->bytes));
   }
   CUDA_TRY(upload(&h->long_bits, lbits.data(), lbits.size() * 4, &h->bytes));
 
@@ -517,7 +516,12 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // one 64-bit load per 4 columns; the W % 4 tail keeps the SELL layout).
   // Same slots, same per-slice positions; slices narrowed by a long row keep
   // the reference layout. A derived device layout, never a parity object.
-  h->ell_vec = C == 32 && env_double("EHYB_VEC", 0.0) != 0.0 && env_double("EHYB_RING", 0.0) == 0.0;
+  // default: fp32 slabs interleaved (4-byte values and 2-byte columns fetch 128 /
+  // 64 B per warp instruction in the SELL layout, below the rate the HBM
+  // stream needs: profiles/stream_probe_r2.txt; cfg3 fp32 114.9 vs 119.2 us),
+  // fp64 in the reference's SELL layout (cfg2 equal, cfg5 992 vs 1031 us)
+  h->ell_vec = C == 32 && env_double("EHYB_VEC", tb == 4 ? 1.0 : 0.0) != 0.0 &&
+               env_double("EHYB_RING", 0.0) == 0.0;
   if (h->ell_vec) {
     std::vector<char> pv(size_t(std::max<int64_t>(slots, 1)) * tb);
     std::vector<uint16_t> pc(size_t(std::max<int64_t>(slots, 1)));
@@ -568,6 +572,16 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     }
     (halo ? hmembers : members)[size_t(r / vec - p0)].push_back(j);
   }
+  // slices holding an ER row publish their completion (the ER add waits on
+  // it); the others skip the fence and the shared-memory atomic (C == 32)
+  if (C == 32) {
+    for (const auto* grp : {&members, &hmembers})
+      for (const auto& mem : *grp)
+        for (int64_t j : mem) eff[size_t((m->y_idx_er[j] - row_lo) / C)] |= kEffHasEr;
+  } else {
+    for (auto& e : eff) e |= kEffHasEr;
+  }
+  CUDA_TRY(upload(&h->width_ell, eff.data(), eff.size() * 4, &h->bytes));
   std::unordered_map<int64_t, int64_t> halo_index;
   halo_index.reserve(size_t(n_halo) * 2 + 1);
   for (int64_t i = 0; i < n_halo; ++i) halo_index[halo_cols[i]] = h->local_rows + i;

@@ -143,6 +143,7 @@ struct SpmvParams {
 
 // ell_eff (the slice widths the kernel reads) = effective width | flags
 constexpr int32_t kEffWidth = 0x00ffffff;
+constexpr int32_t kEffHasEr = 1 << 28;    // a row of the slice has ER entries (publish its completion)
 constexpr int32_t kEffPadTail = 1 << 29;  // lanes owe the reference's padding products 0*win[0]
 constexpr int32_t kEffHasLong = 1 << 30;  // a lane of the slice is a long row (long_bits)
 // lr_row flags
@@ -1030,7 +1031,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   __shared__ int next_er;
   __shared__ int next_comb;
   __shared__ int next_pcomb;
-  __shared__ int ell_finished;
   __shared__ uint32_t chunk_done[kMaxChunks / 32];
   __shared__ uint32_t er_done[kMaxErBuf / 32];
   __shared__ __align__(16) T lr_stage[64];  // long-row products (warp 0)
@@ -1096,7 +1096,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     next_er = 0;
     next_comb = 0;
     next_pcomb = 0;
-    ell_finished = 0;
     if (P.pool_done)  // the next launch's counter of this partition
       P.pool_done[((ep + 1u) & 1u) * uint32_t(P.n_parts) + uint32_t(part)] = 0u;
   }
@@ -1242,11 +1241,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     __syncwarp();
     if (lane == 0) {
       atomicOr(&chunk_done[unpublished >> 5], 1u << (unpublished & 31));
-      // the warp publishing the partition's last chunk publishes the whole
-      // ELL phase to other CTAs (pooled ER rows): one gpu-scope fence per
-      // CTA instead of one per chunk
-      const int fin = atomicAdd(&ell_finished, 1);
-      if (P.timing && fin == int(n_chunks) - 1) P.timing[8 * cta + 7] = globaltimer();
+      if (P.timing) atomicMax(P.timing + 8 * cta + 7, globaltimer());  // dev: last publication
     }
     unpublished = -1;
   };
@@ -1282,6 +1277,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       }
       publish();
       if (store) P.y[row0 + chunk * 32 + lane] = acc;
+      // only slices with an ER row are waited on (wait_chunk / own_pre)
+      unpublished = (m.eff & kEffHasEr) ? chunk : -1;
     } else {
       const int64_t lr = chunk * 32 + lane;
       T acc = T(0);
@@ -1298,8 +1295,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       }
       publish();
       if (!skip) P.y[row0 + lr] = acc;
+      unpublished = chunk;
     }
-    unpublished = chunk;
   };
   auto er_meta = [&](int64_t s, int64_t s_end) { return er_claimed_meta(P, s, s_end, lane); };
   // a row whose ELL value is already final has y read before the slice's

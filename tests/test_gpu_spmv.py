@@ -40,14 +40,21 @@ def small_e(name):
 @pytest.mark.parametrize("name", sorted(small_meta()))
 def test_small_bitwise_numpy_path(name):
     meta, g, m, plan, e = small_e(name)
-    y, stats = E.spmv_ehyb(e, E.permute_vector(g["x"], plan))
+    exact = E.ExecutionConfig(exact=True)
+    y, stats = E.spmv_ehyb(e, E.permute_vector(g["x"], plan), exact)
     assert y.dtype == g["y_reordered"].dtype
     assert y.tobytes() == g["y_reordered"].tobytes()
     assert stats.cached_loads == meta["cached_loads"]
     assert stats.uncached_loads == meta["uncached_loads"]
     assert stats.bytes_touched_model == meta["bytes_touched_model"]
-    yu = E.spmv_ehyb_user(e, g["x"])
+    yu = E.spmv_ehyb_user(e, g["x"], exact)
     assert yu.tobytes() == g["y_user"].tobytes()
+    # default mode: bitwise unless a row is wider than the long-row threshold
+    yd, _ = E.spmv_ehyb(e, E.permute_vector(g["x"], plan))
+    if E.device_matrix(e).info()["long_rows"] == 0:
+        assert yd.tobytes() == y.tobytes()
+    else:
+        assert rel_error(yd, y) <= (1e-12 if meta["tau"] == 8 else 1e-5)
 
 
 @pytest.mark.parametrize("name", sorted(small_meta()))
@@ -58,7 +65,7 @@ def test_small_torch_path_and_fma(name):
     dm = E.device_matrix(e, 0)
     xr = dm.permute(x)
     assert np.array_equal(xr.cpu().numpy(), E.permute_vector(g["x"], plan).astype(xr.cpu().numpy().dtype))
-    y = dm.spmv(xr)
+    y = dm.spmv(xr, exact=True)
     torch.cuda.synchronize()
     assert y.cpu().numpy().tobytes() == g["y_reordered"].tobytes()
     yu = E.unpermute_vector(y, plan)
