@@ -170,6 +170,9 @@ typedef struct ehyb_dev_info {
   int32_t smem_bytes;         /* dynamic shared memory of a fused launch */
   int64_t long_rows;          /* rows computed by the long-row path (width > EHYB_LONG_ROW) */
   int64_t ring_bytes;         /* shared-memory ring the ELL stream is TMA-staged through (0 = off) */
+  int64_t work_units;         /* CTA work units of a launch: partitions x split */
+  int32_t split;              /* units per partition (chunk ranges of one window; EHYB_SPLIT) */
+  int32_t reserved;
 } ehyb_dev_info;
 
 /* Upload an assembled matrix once (device = CUDA ordinal) and derive the

@@ -71,7 +71,8 @@ class DevInfo(C.Structure):
         ("window_bytes", C.c_int64), ("window_in_smem", C.c_int32),
         ("threads_per_cta", C.c_int32), ("ctas", C.c_int32), ("sm_count", C.c_int32),
         ("pool_slices", C.c_int64), ("er_buf_slices", C.c_int32), ("smem_bytes", C.c_int32),
-        ("long_rows", C.c_int64), ("ring_bytes", C.c_int64),
+        ("long_rows", C.c_int64), ("ring_bytes", C.c_int64), ("work_units", C.c_int64),
+        ("split", C.c_int32), ("reserved", C.c_int32),
     ]
 
 

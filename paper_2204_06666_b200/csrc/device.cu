@@ -146,7 +146,9 @@ struct ehyb_dev {
   int32_t* st_chunks = nullptr;
   uint2* ch_stage = nullptr;
   int ell_ahead = 1, er_ahead = 1;
-  int phase_skip = 0;  // EHYB_TUNE_PHASES (dev): bit 0 skips the ER work, bit 1 the ELL stream
+  int phase_skip = 0;
+  int32_t split = 1, unit_chunks = 0;  // work units per partition, chunks per unit
+  int64_t n_units = 0;                 // launch work units (partitions x split)  // EHYB_TUNE_PHASES (dev): bit 0 skips the ER work, bit 1 the ELL stream
   // ER padding column (SURVEY.md 8a gotcha 4): x index of the column the
   // reference's padding slots hold; shards without it locally fix up later
   int64_t er_pad_idx = 0;
@@ -259,7 +261,9 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.er_buf_slices = h->er_buf_slices;
   P.er_buf_offset = h->er_buf_offset;
   P.er_warps = h->er_warps;
-  P.n_parts = int32_t(h->local_rows / h->vec);
+  P.n_parts = int32_t(h->n_units);
+  P.split = h->split;
+  P.unit_chunks = h->unit_chunks;
   P.ell_ahead = h->ell_ahead;
   P.er_ahead = h->er_ahead;
   P.long_bits = h->long_bits;
@@ -330,8 +334,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
     }
   }
   // at most one wave of resident CTAs; each loops over its partitions
-  const int64_t n_local_parts = h->local_rows / h->vec;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(n_local_parts, h->max_ctas));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(h->n_units, h->max_ctas));
 
   // cooperative launch: the runtime guarantees every CTA of the grid is
   // resident at once (or fails the launch) — the pool, persistent-group and
@@ -633,6 +636,38 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // other CTAs' ELL publication) cannot deadlock
   const bool pool_ok = true;
 
+  // work units: a shard with fewer partitions than resident CTAs (a rank that
+  // owns 74 of cfg5's 592 partitions on 148 SMs) splits each partition's
+  // 32-row chunks into `split` contiguous units, one CTA each; every unit
+  // stages the partition's window (SURVEY.md 8e option (i): the structure
+  // stays that of the 1-GPU profile at every GPU count)
+  int64_t split = 1;
+  if (C == 32 && env_double("EHYB_RING", 0.0) == 0.0) {
+    const double forced = env_double("EHYB_SPLIT", 0.0);
+    if (forced >= 1.0) split = int64_t(forced);
+    else if (n_loc_parts < h->max_ctas)
+      split = std::min<int64_t>(std::min<int64_t>(4, h->max_ctas / n_loc_parts), chunks / 8);
+    split = std::max<int64_t>(1, std::min<int64_t>(split, chunks));
+  }
+  const int64_t unit_chunks = (chunks + split - 1) / split;
+  split = (chunks + unit_chunks - 1) / unit_chunks;  // no empty unit
+  h->split = int32_t(split);
+  h->unit_chunks = int32_t(unit_chunks);
+  const int64_t n_units = n_loc_parts * split;
+  h->n_units = n_units;
+  if (split > 1) {  // regroup the per-partition ER members by unit (order kept)
+    auto unit_of = [&](int64_t lr) {
+      const int64_t q = lr / vec;
+      return q * split + std::min<int64_t>(((lr - q * vec) >> 5) / unit_chunks, split - 1);
+    };
+    for (auto* grp : {&members, &hmembers}) {
+      std::vector<std::vector<int64_t>> by_unit(static_cast<size_t>(n_units));
+      for (const auto& mem : *grp)
+        for (int64_t j : mem) by_unit[size_t(unit_of(m->y_idx_er[j] - row_lo))].push_back(j);
+      grp->swap(by_unit);
+    }
+  }
+
   // per-partition 32-row ER slices (members in reference order), then the
   // own / pool split: partition q keeps the prefix of its ER slices that fits
   // its share of the mean per-CTA cost (ELL slots + er_cost * ER entries);
@@ -648,18 +683,20 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   }
   const double pool_factor = env_double("EHYB_POOL_FACTOR", small ? 1e30 : 0.95);
   const double er_cost = env_double("EHYB_ER_COST", 5.0);
-  std::vector<double> ell_cost(static_cast<size_t>(n_loc_parts)), er_total(static_cast<size_t>(n_loc_parts), 0.0);
+  std::vector<double> ell_cost(static_cast<size_t>(n_units)), er_total(static_cast<size_t>(n_units), 0.0);
   double total = 0.0;
-  for (int64_t q = 0; q < n_loc_parts; ++q) {
-    const int64_t a = (q * vec) / C, b = ((q + 1) * vec) / C;
+  for (int64_t q = 0; q < n_units; ++q) {
+    const int64_t qp = q / split, c0 = (q % split) * unit_chunks;
+    const int64_t a = (qp * vec) / C + c0 * (32 / C),
+                  b = std::min<int64_t>(((qp + 1) * vec) / C, a + unit_chunks * (32 / C));
     ell_cost[size_t(q)] = double(pos[size_t(b)] - pos[size_t(a)]);
     for (int64_t j : members[size_t(q)]) er_total[size_t(q)] += er_cost * m->er_row_widths[j];
     total += ell_cost[size_t(q)] + er_total[size_t(q)];
   }
-  const double budget_mean = n_loc_parts ? total / double(n_loc_parts) : 0.0;
+  const double budget_mean = n_units ? total / double(n_units) : 0.0;
   struct SliceRef { int64_t q, i0; bool halo; };
-  std::vector<std::vector<SliceRef>> own(static_cast<size_t>(n_loc_parts)), spill(static_cast<size_t>(n_loc_parts));
-  for (int64_t q = 0; q < n_loc_parts; ++q) {
+  std::vector<std::vector<SliceRef>> own(static_cast<size_t>(n_units)), spill(static_cast<size_t>(n_units));
+  for (int64_t q = 0; q < n_units; ++q) {
     const auto& mem = members[size_t(q)];
     double left = (pool_ok && pool_factor > 0.0) ? pool_factor * budget_mean - ell_cost[size_t(q)]
                                                  : 1e300;
@@ -676,9 +713,9 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       }
     }
   }
-  std::vector<int32_t> part_ptr(size_t(n_loc_parts) + 1, 0), part_mid(static_cast<size_t>(n_loc_parts), 0);
+  std::vector<int32_t> part_ptr(size_t(n_units) + 1, 0), part_mid(static_cast<size_t>(n_units), 0);
   std::vector<SliceRef> order;
-  for (int64_t q = 0; q < n_loc_parts; ++q) {
+  for (int64_t q = 0; q < n_units; ++q) {
     for (const auto& r : own[size_t(q)]) order.push_back(r);
     part_mid[size_t(q)] = int32_t(order.size());
     for (size_t i0 = 0; i0 < hmembers[size_t(q)].size(); i0 += 32) order.push_back({q, int64_t(i0), true});
@@ -687,7 +724,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->pool_lo = int64_t(order.size());
   for (size_t round = 0;; ++round) {  // pool: round-robin over the heavy partitions
     bool any = false;
-    for (int64_t q = 0; q < n_loc_parts; ++q)
+    for (int64_t q = 0; q < n_units; ++q)
       if (round < spill[size_t(q)].size()) {
         order.push_back(spill[size_t(q)][round]);
         any = true;
@@ -699,10 +736,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // the iteration in which the owner partition runs on its CTA (q / grid)
   std::vector<int32_t> pool_gptr;
   bool own_scratch = false;
-  if (n_loc_parts > h->max_ctas && h->pool_hi > h->pool_lo &&
+  if (n_units > h->max_ctas && h->pool_hi > h->pool_lo &&
       env_double("EHYB_POOL_DIRECT", 1.0) != 0.0) {
     const int64_t grid = h->max_ctas;
-    const int64_t ng = (n_loc_parts + grid - 1) / grid;
+    const int64_t ng = (n_units + grid - 1) / grid;
     std::stable_sort(order.begin() + h->pool_lo, order.end(),
                      [&](const SliceRef& a, const SliceRef& b) { return a.q / grid < b.q / grid; });
     pool_gptr.assign(static_cast<size_t>(ng) + 1, 0);
@@ -712,7 +749,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   }
   {
     int64_t max_own = 0;
-    for (int64_t q = 0; q < n_loc_parts; ++q) max_own = std::max<int64_t>(max_own, int64_t(own[size_t(q)].size()));
+    for (int64_t q = 0; q < n_units; ++q) max_own = std::max<int64_t>(max_own, int64_t(own[size_t(q)].size()));
     h->er_buf_slices = int(std::min<int64_t>(h->er_buf_slices, max_own));
     // partitions with more own ER slices than the shared-memory buffer holds
     // (large windows, e.g. cfg5) spill the rest to a global scratch, so the
@@ -984,9 +1021,9 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   }
   // ---- ER pool state: claim counters, per-owner lists, scratch, counts
   if (h->pool_hi > h->pool_lo) {
-    std::vector<int32_t> optr(static_cast<size_t>(n_loc_parts) + 1, 0), oidx;
+    std::vector<int32_t> optr(static_cast<size_t>(n_units) + 1, 0), oidx;
     for (int64_t sl = h->pool_lo; sl < h->pool_hi; ++sl) optr[size_t(order[size_t(sl)].q) + 1] += 1;
-    for (int64_t q = 0; q < n_loc_parts; ++q) optr[size_t(q) + 1] += optr[size_t(q)];
+    for (int64_t q = 0; q < n_units; ++q) optr[size_t(q) + 1] += optr[size_t(q)];
     oidx.resize(size_t(h->pool_hi - h->pool_lo));
     std::vector<int32_t> fill(optr.begin(), optr.end() - 1);
     for (int64_t sl = h->pool_lo; sl < h->pool_hi; ++sl)
@@ -995,11 +1032,11 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     CUDA_TRY(upload(&h->pool_own_idx, oidx.data(), oidx.size() * 4, &h->bytes));
     const size_t acc_bytes = size_t(h->pool_hi - h->pool_lo) * 32 * tb;
     CUDA_TRY(cudaMalloc(&h->pool_acc, acc_bytes));
-    CUDA_TRY(cudaMalloc(&h->pool_done, size_t(n_loc_parts) * 8 + 16));
-    CUDA_TRY(cudaMemset(h->pool_done, 0, size_t(n_loc_parts) * 8 + 16));
+    CUDA_TRY(cudaMalloc(&h->pool_done, size_t(n_units) * 8 + 16));
+    CUDA_TRY(cudaMemset(h->pool_done, 0, size_t(n_units) * 8 + 16));
     CUDA_TRY(cudaMalloc(&h->pool_ctr, 16));
     CUDA_TRY(cudaMemset(h->pool_ctr, 0, 16));
-    h->bytes += acc_bytes + size_t(n_loc_parts) * 8 + 32;
+    h->bytes += acc_bytes + size_t(n_units) * 8 + 32;
     if (!pool_gptr.empty()) {
       const int64_t ng = int64_t(pool_gptr.size()) - 1;
       h->pool_groups = int32_t(ng);
@@ -1007,9 +1044,9 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       CUDA_TRY(upload(&h->pool_grp, pool_gptr.data(), pool_gptr.size() * 4, &h->bytes));
       CUDA_TRY(cudaMalloc(&h->pool_gctr, size_t(ng) * 8 + 16));
       CUDA_TRY(cudaMemset(h->pool_gctr, 0, size_t(ng) * 8 + 16));
-      CUDA_TRY(cudaMalloc(&h->part_flag, size_t(n_loc_parts) * 4 + 16));
-      CUDA_TRY(cudaMemset(h->part_flag, 0, size_t(n_loc_parts) * 4 + 16));
-      h->bytes += size_t(ng) * 12 + size_t(n_loc_parts) * 4 + 48;
+      CUDA_TRY(cudaMalloc(&h->part_flag, size_t(n_units) * 4 + 16));
+      CUDA_TRY(cudaMemset(h->part_flag, 0, size_t(n_units) * 4 + 16));
+      h->bytes += size_t(ng) * 12 + size_t(n_units) * 4 + 48;
     }
   }
   *out = h.release();
@@ -1079,7 +1116,10 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out) {
   out->window_bytes = h->vec * h->tau;
   out->window_in_smem = h->window_in_smem ? 1 : 0;
   out->threads_per_cta = h->threads;
-  out->ctas = int32_t(std::min<int64_t>(h->local_rows / h->vec, h->max_ctas));
+  out->ctas = int32_t(std::min<int64_t>(h->n_units, h->max_ctas));
+  out->work_units = h->n_units;
+  out->split = h->split;
+  out->reserved = 0;
   out->sm_count = h->sm_count;
   out->pool_slices = h->pool_hi - h->pool_lo;
   out->er_buf_slices = h->er_buf_slices;

@@ -108,7 +108,11 @@ struct SpmvParams {
   int32_t er_buf_slices;            // buffered own ER slices (<= kMaxErBuf)
   int32_t er_buf_offset;            // byte offset of the buffer in dynamic smem
   int32_t er_warps;                 // warps that start on ER before ELL
-  int32_t n_parts;                  // partitions of this launch (grid may be smaller: CTAs loop)
+  int32_t n_parts;                  // work units of this launch (grid may be smaller: CTAs loop)
+  int32_t split;                    // units per partition (a partition's 32-row chunks split
+                                    // into `split` contiguous ranges, each its own CTA that
+                                    // stages the same window; 1 = one unit per partition)
+  int32_t unit_chunks;              // chunks per unit (the last unit of a partition may be short)
   int32_t ell_vec;                  // 1: ELL slices in the 128-bit interleaved layout
   int32_t ring_offset;              // RING variant: ELL staging ring in dynamic smem,
   int32_t ring_stages, stage_bytes, stage_vbytes;  // stages x stage_bytes (values first)
@@ -140,6 +144,16 @@ struct SpmvParams {
   unsigned int* lr_cnt;                    // [tasks] finished segments (self-resetting)
   unsigned int* lr_ctr;                    // [2] task / segment claim counters by epoch
 };
+
+// The work unit that owns (local) row r: partition r / vec, chunk range by
+// unit_chunks (SpmvParams::split).
+template <typename T>
+__device__ __forceinline__ uint32_t unit_of_row(const SpmvParams<T>& P, uint32_t r) {
+  const uint32_t q = r / uint32_t(P.vec);
+  if (P.split == 1) return q;
+  const uint32_t h = ((r - q * uint32_t(P.vec)) >> 5) / uint32_t(P.unit_chunks);
+  return q * uint32_t(P.split) + (h < uint32_t(P.split) ? h : uint32_t(P.split) - 1u);
+}
 
 // ell_eff (the slice widths the kernel reads) = effective width | flags
 constexpr int32_t kEffWidth = 0x00ffffff;
@@ -827,7 +841,7 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     const T acc = er_slice_compute<T, STRICT>(P, m);
     P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc;
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
-    const uint32_t owner = uint32_t(rw0 & kRowMask) / uint32_t(P.vec);
+    const uint32_t owner = unit_of_row(P, uint32_t(rw0 & kRowMask));
     if (n_pend == 0) pend0 = owner;
     else if (n_pend == 1) pend1 = owner;
     else if (n_pend == 2) pend2 = owner;
@@ -863,8 +877,8 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     __syncwarp();
     const int32_t ra = __shfl_sync(0xffffffffu, ma.rw, 0), rb = __shfl_sync(0xffffffffu, mb.rw, 0);
     if (lane == 0) {
-      atomicAdd(done + uint32_t(ra & kRowMask) / uint32_t(P.vec), 1u);
-      if (two) atomicAdd(done + uint32_t(rb & kRowMask) / uint32_t(P.vec), 1u);
+      atomicAdd(done + unit_of_row(P, uint32_t(ra & kRowMask)), 1u);
+      if (two) atomicAdd(done + unit_of_row(P, uint32_t(rb & kRowMask)), 1u);
     }
   }
   } else {
@@ -897,7 +911,7 @@ __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, 
   auto finish = [&](const ErMeta& m, T acc) {
     if (m.rw < 0) return;
     const uint32_t r = uint32_t(m.rw & kRowMask);
-    const uint32_t owner = r / uint32_t(P.vec);
+    const uint32_t owner = unit_of_row(P, r);
     while (ld_acquire_gpu(P.part_flag + owner) != ep) __nanosleep(64);
     P.y[r] = add_rn(__ldcg(P.y + r), acc);
   };
@@ -943,7 +957,7 @@ __device__ void pool_scratch_group(const SpmvParams<T>& P, int lane, uint32_t ep
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
     __threadfence();
     __syncwarp();
-    if (lane == 0) atomicAdd(done + uint32_t(rw0 & kRowMask) / uint32_t(P.vec), 1u);
+    if (lane == 0) atomicAdd(done + unit_of_row(P, uint32_t(rw0 & kRowMask)), 1u);
   }
 }
 
@@ -1037,7 +1051,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int cta = blockIdx.x;
-  const int64_t n_chunks = (P.vec + 31) >> 5;
+  const int64_t part_chunks = (P.vec + 31) >> 5;
   T* xs = reinterpret_cast<T*>(smem_raw);
 
   __shared__ uint32_t s_ep;
@@ -1080,8 +1094,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   // slices of its partition computes pooled slices itself, and computing a
   // pooled slice never waits, so the wait always ends.
   for (int it = 0, part = cta; part < P.n_parts; ++it, part += gridDim.x) {
-  const int64_t row0 = int64_t(part) * P.vec;
-  const T* xwin = P.x + row0;
+  // unit `part` = chunks [c0, c0 + n_chunks) of partition q; row0 is the
+  // unit's first row, the window is the whole partition's
+  const int64_t q = part / P.split;
+  const int64_t c0 = int64_t(part - q * P.split) * P.unit_chunks;
+  const int64_t n_chunks = (part_chunks - c0 < P.unit_chunks ? part_chunks - c0 : P.unit_chunks);
+  const int64_t unit_rows = (P.vec - c0 * 32 < n_chunks * 32 ? P.vec - c0 * 32 : n_chunks * 32);
+  const int64_t row0 = q * P.vec + c0 * 32;
+  const T* xwin = P.x + q * P.vec;
   const int64_t s0 = P.er_sel == 2 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part);
   const int64_t s1 = P.er_sel == 1 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part + 1);
   const uint32_t phase = uint32_t(it) & 1u;
@@ -1282,7 +1302,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     } else {
       const int64_t lr = chunk * 32 + lane;
       T acc = T(0);
-      bool skip = lr >= P.vec;
+      bool skip = lr >= unit_rows;
       if (!skip) {
         const int64_t r = row0 + lr;
         const int64_t C = P.warp;

@@ -9,5 +9,5 @@ std::string& error_slot() {
 
 extern "C" {
 EHYB_API const char* ehyb_last_error(void) { return ehyb::error_slot().c_str(); }
-EHYB_API int ehyb_abi_version(void) { return 1; }
+EHYB_API int ehyb_abi_version(void) { return 2; }
 }

@@ -397,6 +397,12 @@ class DistributedEhyb:
             self, lambda ptrs: [lib.ehyb_ipc_close(C.c_void_p(p)) for p in ptrs],
             list(self._peer_ptrs))
 
+    def info(self) -> dict:
+        """ehyb_dev_info of this rank's handle (grid, work units, split, ...)."""
+        out = L.DevInfo()
+        L.call("ehyb_dev_info_get", self._h, C.byref(out))
+        return {f: getattr(out, f) for f, _ in L.DevInfo._fields_}
+
     def new_ext(self):
         """A fresh zeroed x in the [owned | halo] layout the SpMV reads."""
         import torch
@@ -588,6 +594,75 @@ def weak_config(world: int):
     return W.permute_symmetric(*W.stencil27(128 * world, 128, 128), seed=1)
 
 
+def dist_workload(name: str, world: int):
+    """The multi-rank bench workload: (n, rows, cols, vals, tau, profile, desc).
+    A named config (default cfg5, BASELINE configs[4]) keeps its 1-GPU
+    profile at every GPU count, so every N streams the same structure and
+    bytes (SURVEY.md 8e option (i)); ranks that own fewer partitions than
+    SMs split them into work units. "weak": the 128*N x 128 x 128 permuted
+    stencil with P = 148*N (N = 1 is cfg2)."""
+    from . import workloads as W
+    from .format import DeviceProfile, b200_profile
+
+    if name == "weak":
+        n, r, c, v = weak_config(world)
+        return (n, r, c, v, 8, b200_profile(world),
+                f"27-point stencil {128 * world}x128x128, random symmetric permutation, "
+                f"P=148x{world} (weak scaling; N=1: cfg2)")
+    if name not in W.CONFIGS:
+        raise ValueError(f"unknown config {name!r}")
+    n, r, c, v, tau = W.build_config(name)
+    prof = W.CONFIG_PROFILES.get(name)
+    return (n, r, c, v, tau, DeviceProfile(*prof) if prof else b200_profile(1),
+            f"{name}: {W.CONFIGS[name][0]}")
+
+
+def single_gpu_reference(e, device: int, args):
+    """The same matrix on this one GPU (rank 0, before sharding): the T_1 of
+    the strong-scaling run, CUDA-event time per SpMV."""
+    import torch
+
+    from .device import DeviceMatrix
+    from .format import permute_vector
+    from . import workloads as W
+
+    dm = DeviceMatrix(e, device)
+    xr = torch.from_numpy(permute_vector(W.deterministic_vector(e.dimension, 0), e.plan)).to(
+        f"cuda:{device}", dm.torch_dtype)
+    y = torch.empty_like(xr)
+    for _ in range(max(3, args.warmup)):
+        dm.spmv(xr, y)
+    torch.cuda.synchronize()
+    k = max(10, min(args.steps, 100))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(k):
+        dm.spmv(xr, y)
+    b.record()
+    b.synchronize()
+    t = a.elapsed_time(b) / 1e3 / k
+    out = {"ms_per_step": t * 1e3, "value": 2 * e.nnz / t / 1e9, "unit": "GFLOP/s",
+           "ctas": dm.info()["ctas"], "how": "the same assembled matrix on rank 0's GPU alone "
+                                             "(T_1 of this strong-scaling run)"}
+    dm.close()
+    del xr, y
+    torch.cuda.empty_cache()
+    return out
+
+
+def measured_hbm_peak():
+    """MEASURED_PEAKS.json hbm_gbs (driver-written), else the B200 recipe's
+    fallback."""
+    import json
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    try:
+        with open(os.path.join(root, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001 - absent on a fresh box
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
 def bench_main(args, clock_cls=None):
     import json
 
@@ -624,21 +699,28 @@ def bench_main(args, clock_cls=None):
         sys.stdout.flush()
         os.dup2(saved, 1)
         os.close(saved)
-    path = os.path.join(os.environ.get("EHYB_SCRATCH", "/tmp"), f"ehyb_weak_{world}.ehyb")
+    name = getattr(args, "config", None) or "cfg5"
+    path = os.path.join(os.environ.get("EHYB_SCRATCH", "/tmp"), f"ehyb_{name}_{world}.ehyb")
     t0 = time.perf_counter()
     nnz = None
+    single = None
     if rank == 0:
-        n, r, c, v = weak_config(world)
+        n, r, c, v, tau, prof, desc = dist_workload(name, world)
         m = CooMatrix(n, n, r, c, v)
         nnz = m.nnz
-        e = build_ehyb(m, tau=8, profile=b200_profile(world))
+        del r, c, v
+        e = build_ehyb(m, tau=tau, profile=prof)
+        del m
+        if world > 1 and name != "weak":
+            single = single_gpu_reference(e, local, args)
         # contiguous rank blocks of a quotient-graph ordering of the partitions
         e = renumber_partitions(e, group_partitions(e, world))
         write_ehyb_container(e, path)
-        del m, r, c, v
-    obj = [nnz]
+    else:
+        desc = None
+    obj = [nnz, desc]
     dist.broadcast_object_list(obj, src=0)
-    nnz = obj[0]
+    nnz, desc = obj
     dist.barrier()
     if rank != 0:
         e = read_ehyb_container(path)
@@ -663,6 +745,9 @@ def bench_main(args, clock_cls=None):
     # the other exchange, timed beside it (N > 1)
     A_nccl = DistributedEhyb(e, device=local) if (exchange == "p2p" and world > 1) else None
     bmin_total = engine.min_bytes(e)
+    n_parts = e.n_parts
+    info0 = A.info()
+    peak, peak_src = measured_hbm_peak()
     e_full = e if rank == 0 else None  # the single-GPU product checks the sharded one
     from . import workloads as W
 
@@ -791,19 +876,22 @@ def bench_main(args, clock_cls=None):
             "metric": "SpMV GFLOP/s (2*nnz/t) and achieved HBM GB/s vs peak",
             "value": flops / t_step / 1e9, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if name == "weak" else "strong",
+            "vs_baseline": None, "dtype": "f64" if A.tau == 8 else "f32",
             "data": "synthetic",
-            "config": {"workload": f"27-point stencil {128 * world}x128x128, random symmetric "
-                                   f"permutation, P=148x{world} (N=1: cfg2; N=8: cfg5 rows)",
-                       "nnz": nnz, "parallelism": (
+            "config": {"workload": desc, "n": int(A.plan.vec * n_parts), "nnz": nnz,
+                       "n_parts": n_parts, "work_units_rank0": info0["work_units"],
+                       "split_rank0": info0["split"], "parallelism": (
                            f"row shards x{world}, halo pulled from peer memory inside one "
                            f"fused launch" if exchange == "p2p" else
                            f"row shards x{world}, NCCL halo all-to-all overlapped with the "
                            f"local launch"),
                        "l2_policy": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": bmin_total / t_step / 1e9 / world,
-                         "peak": 6457.4, "unit": "GB/s (per GPU)",
-                         "frac": bmin_total / t_step / 1e9 / world / 6457.4, "traffic": None},
+                         "peak": peak, "unit": "GB/s (per GPU)", "peak_source": peak_src,
+                         "frac": bmin_total / t_step / 1e9 / world / peak, "traffic": None,
+                         "algorithmic_bytes_per_step": bmin_total},
+            "same_matrix_1gpu": single,
             "e2e": {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s",
                     "h2d_bytes_per_step": int(nb), "d2h_bytes_per_step": int(nb),
                     "ms_per_step": t_e2e * 1e3,

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for n in declared():
         assert isinstance(getattr(lib, n), ctypes._CFuncPtr)
     assert sorted(L.exported_symbols()) == declared()
-    assert lib.ehyb_abi_version() == 1
+    assert lib.ehyb_abi_version() == 2
     assert lib.ehyb_num_threads() >= 1
 
 

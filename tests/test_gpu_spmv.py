@@ -416,3 +416,42 @@ def test_fused_launch_beside_busy_kernels():
         torch.cuda.synchronize()
         for y in ys:
             assert y.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("split", [1, 2, 3, 4])
+@pytest.mark.parametrize("tau", [4, 8])
+def test_work_units_split_partitions(monkeypatch, split, tau):
+    # a partition's chunks split over `split` CTAs (each stages the window):
+    # the multi-GPU path when a rank owns fewer partitions than SMs. Bitwise
+    # on the pool, persistent and shard paths, long rows included
+    from paper_2204_06666_b200 import distributed as D
+    from paper_2204_06666_b200.device import DeviceMatrix
+
+    monkeypatch.setenv("EHYB_SPLIT", str(split))
+    monkeypatch.setenv("EHYB_LONG_ROW", "60")
+    n, r, c, v = W.heavy_tail(k=20, n_hubs=3, min_len=100, max_len=900)
+    for prof in (E.DeviceProfile(6, 32, 16384), E.DeviceProfile(400, 32, 2048)):
+        e = E.build_ehyb(E.CooMatrix(n, n, r, c, v), tau=tau, profile=prof)
+        dm = DeviceMatrix(e, 0)
+        info = dm.info()
+        assert info["split"] >= 1 and info["work_units"] == e.n_parts * info["split"]
+        if prof.num_processors == 6:
+            assert info["split"] == min(split, (e.params.vec_cache_size + 31) // 32)
+        xr = E.permute_vector(W.deterministic_vector(n, split), e.plan)
+        want = c_oracle.spmv_ehyb(e, xr)
+        xt = torch.from_numpy(xr).to("cuda:0", dm.torch_dtype)
+        for _ in range(2):
+            assert dm.spmv(xt, exact=True).cpu().numpy().tobytes() == want.tobytes()
+        dm.close()
+        for world in (2, 3):
+            for rank in range(world):
+                plan = D.plan_for(e, rank, world)
+                A = D.DistributedEhyb(e, device=0, plan=plan)
+                lo, hi = plan.p0 * plan.vec, plan.p1 * plan.vec
+                x_ext = A.new_ext()
+                x_ext[: plan.local_rows] = torch.from_numpy(xr[lo:hi]).to(A.dtype)
+                x_ext[plan.local_rows:] = torch.from_numpy(xr[plan.halo_cols]).to(A.dtype)
+                ys = torch.empty(plan.local_rows, dtype=A.dtype, device="cuda:0")
+                A.spmv_local(x_ext, ys, exact=True)
+                torch.cuda.synchronize()
+                assert ys.cpu().numpy().tobytes() == want[lo:hi].tobytes()
