@@ -117,6 +117,7 @@ def build_workload(name: str):
     params = E.compute_params(n, tau, E.DeviceProfile(*prof) if prof else E.B200_PROFILE)
     t0 = time.perf_counter()
     g = E.build_graph(m)
+    tg = time.perf_counter()
     parts = E.partition_graph(g, params.n_parts, params.vec_cache_size, seed=0)
     t1 = time.perf_counter()
     cls = E.classify_rows(m, parts)
@@ -124,7 +125,8 @@ def build_workload(name: str):
     e = E.assemble_ehyb(m, plan, params, parts)
     t2 = time.perf_counter()
     del g, cls
-    return m, e, dict(generate_s=t_gen, partition_s=t1 - t0, reorder_assemble_s=t2 - t1)
+    return m, e, dict(generate_s=t_gen, partition_s=t1 - t0, reorder_assemble_s=t2 - t1,
+                      build_graph_s=tg - t0, partition_graph_s=t1 - tg)
 
 
 def golden_y_digest(name: str):

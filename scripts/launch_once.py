@@ -29,9 +29,12 @@ dm = E.device_matrix(e, 0)
 xr = torch.from_numpy(E.permute_vector(W.deterministic_vector(e.dimension, 0), e.plan)).to(
     "cuda:0", dm.torch_dtype)
 y = torch.empty_like(xr)
-name = {"full": "ehyb_dev_spmv", "ell": "ehyb_dev_spmv_ell", "er": "ehyb_dev_spmv_er"}[args.mode]
+# ell / er: one phase alone (EHYB_TUNE_PHASES, measurement only): the ER-only
+# launch isolates the spill path (its L2 hit rate is the ER x gathers')
+dm.tune(phases={"full": 0, "ell": 1, "er": 2}[args.mode])
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 for _ in range(args.n):
-    L.call(name, dm.handle, C.c_void_p(xr.data_ptr()), C.c_void_p(y.data_ptr()), L.MODE_STRICT, st)
+    L.call("ehyb_dev_spmv", dm.handle, C.c_void_p(xr.data_ptr()), C.c_void_p(y.data_ptr()),
+           L.MODE_DEFAULT, st)
 torch.cuda.synchronize()
 print("done", dm.info())

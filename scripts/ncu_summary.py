@@ -29,6 +29,14 @@ METRICS = [
     ("dram__bytes.sum.per_second", "DRAM throughput"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak (ncu)"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
+    ("lts__t_sector_op_read_hit_rate.pct", "L2 read hit rate"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "barrier stalls / issue"),
+    ("smsp__average_warps_issue_stalled_membar_per_issue_active.ratio", "membar stalls / issue"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+     "short-scoreboard stalls / issue"),
+    ("smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio", "LG-throttle stalls / issue"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
@@ -43,8 +51,12 @@ METRICS = [
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` exported on the GPU box
+        with open(rep) as fh:
+            out = fh.read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     return [dict(zip(hdr, zip(r, units))) for r in rows[2:]]
