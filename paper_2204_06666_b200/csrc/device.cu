@@ -288,9 +288,15 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
     P.part_flag = nullptr;  // no group drains (the group counters still reset)
     P.pool_last_scratch = 0;
   }
-  void (*kern)(const SpmvParams<T>) = (do_ell && h->window_in_smem)
-                                           ? spmv_fused_kernel<T, MODE, C32, true, false>
-                                           : spmv_fused_kernel<T, MODE, C32, false, false>;
+  // work-unit split (several CTAs per partition): its own variant, so the
+  // one-unit-per-partition kernel keeps the register allocation it had
+  const bool split = h->split > 1;
+  void (*kern)(const SpmvParams<T>) =
+      (do_ell && h->window_in_smem)
+          ? (split ? spmv_fused_kernel<T, MODE, C32, true, false, false, true>
+                   : spmv_fused_kernel<T, MODE, C32, true, false>)
+          : (split ? spmv_fused_kernel<T, MODE, C32, false, false, false, true>
+                   : spmv_fused_kernel<T, MODE, C32, false, false>);
   // dynamic smem: [window | own-ER buffer | ELL ring]; the buffer is only
   // used when one launch runs both phases, the ring by any ELL launch
   size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
@@ -314,7 +320,9 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
     }
   }
   if constexpr (C32) {
-    if (h->p2p_active) kern = spmv_fused_kernel<T, MODE, true, true, false, true>;
+    if (h->p2p_active)
+      kern = split ? spmv_fused_kernel<T, MODE, true, true, false, true, true>
+                   : spmv_fused_kernel<T, MODE, true, true, false, true>;
   }
   if (!(do_ell && do_er)) {
     P.er_buf_slices = 0;

@@ -147,10 +147,10 @@ struct SpmvParams {
 
 // The work unit that owns (local) row r: partition r / vec, chunk range by
 // unit_chunks (SpmvParams::split).
-template <typename T>
+template <bool SPLIT, typename T>
 __device__ __forceinline__ uint32_t unit_of_row(const SpmvParams<T>& P, uint32_t r) {
   const uint32_t q = r / uint32_t(P.vec);
-  if (P.split == 1) return q;
+  if constexpr (!SPLIT) return q;
   const uint32_t h = ((r - q * uint32_t(P.vec)) >> 5) / uint32_t(P.unit_chunks);
   return q * uint32_t(P.split) + (h < uint32_t(P.split) ? h : uint32_t(P.split) - 1u);
 }
@@ -809,7 +809,7 @@ __device__ void long_rows_warp(const SpmvParams<T>& P, int lane, T* stage, uint3
 // row sums to the scratch, then count the slice for its owning partition
 // (release: the sums are visible before the count). At most `max_items`
 // slices (<= 0: until the pool is exhausted); returns false once exhausted.
-template <typename T, bool STRICT>
+template <typename T, bool STRICT, bool SPLIT>
 __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint32_t ep) {
   if (P.pool_hi <= P.pool_lo) return false;
   unsigned int* ctr = P.pool_ctr + (ep & 1u);
@@ -841,7 +841,7 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     const T acc = er_slice_compute<T, STRICT>(P, m);
     P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc;
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
-    const uint32_t owner = unit_of_row(P, uint32_t(rw0 & kRowMask));
+    const uint32_t owner = unit_of_row<SPLIT>(P, uint32_t(rw0 & kRowMask));
     if (n_pend == 0) pend0 = owner;
     else if (n_pend == 1) pend1 = owner;
     else if (n_pend == 2) pend2 = owner;
@@ -877,8 +877,8 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     __syncwarp();
     const int32_t ra = __shfl_sync(0xffffffffu, ma.rw, 0), rb = __shfl_sync(0xffffffffu, mb.rw, 0);
     if (lane == 0) {
-      atomicAdd(done + unit_of_row(P, uint32_t(ra & kRowMask)), 1u);
-      if (two) atomicAdd(done + unit_of_row(P, uint32_t(rb & kRowMask)), 1u);
+      atomicAdd(done + unit_of_row<SPLIT>(P, uint32_t(ra & kRowMask)), 1u);
+      if (two) atomicAdd(done + unit_of_row<SPLIT>(P, uint32_t(rb & kRowMask)), 1u);
     }
   }
   } else {
@@ -902,7 +902,7 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
 // published (part_flag == epoch). Group g's owners run in iteration g, and a
 // warp drains group g only after its own CTA has finished iteration g, so
 // every wait is on an earlier-or-equal iteration of another CTA: no cycle.
-template <typename T, bool STRICT>
+template <typename T, bool STRICT, bool SPLIT>
 __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, int g) {
   if (g < 0 || g >= P.pool_groups) return;
   const int64_t lo = __ldg(P.pool_grp + g), hi = __ldg(P.pool_grp + g + 1);
@@ -911,7 +911,7 @@ __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, 
   auto finish = [&](const ErMeta& m, T acc) {
     if (m.rw < 0) return;
     const uint32_t r = uint32_t(m.rw & kRowMask);
-    const uint32_t owner = unit_of_row(P, r);
+    const uint32_t owner = unit_of_row<SPLIT>(P, r);
     while (ld_acquire_gpu(P.part_flag + owner) != ep) __nanosleep(64);
     P.y[r] = add_rn(__ldcg(P.y + r), acc);
   };
@@ -940,7 +940,7 @@ __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, 
 // it (ER-first warps of the last iteration, then anyone after the loop) into
 // the scratch and counted for its owner; the owner CTA adds the sums once
 // its count is complete. Computing never waits.
-template <typename T, bool STRICT>
+template <typename T, bool STRICT, bool SPLIT>
 __device__ void pool_scratch_group(const SpmvParams<T>& P, int lane, uint32_t ep, int g) {
   if (g < 0 || g >= P.pool_groups) return;
   const int64_t lo = __ldg(P.pool_grp + g), hi = __ldg(P.pool_grp + g + 1);
@@ -957,7 +957,7 @@ __device__ void pool_scratch_group(const SpmvParams<T>& P, int lane, uint32_t ep
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
     __threadfence();
     __syncwarp();
-    if (lane == 0) atomicAdd(done + unit_of_row(P, uint32_t(rw0 & kRowMask)), 1u);
+    if (lane == 0) atomicAdd(done + unit_of_row<SPLIT>(P, uint32_t(rw0 & kRowMask)), 1u);
   }
 }
 
@@ -1027,7 +1027,7 @@ constexpr int kMaxErBuf = 2048;                        // buffered own ER slices
 // warp moves straight on to the partition's ER slices (no CTA barrier). An
 // ER row whose ELL chunk is still in flight waits on that chunk's done bit,
 // so y[r] = y_ell[r] + er_acc keeps the reference's order of operations.
-template <typename T, int MODE, bool C32, bool SMEM, bool RING, bool P2P = false>
+template <typename T, int MODE, bool C32, bool SMEM, bool RING, bool P2P = false, bool SPLIT = false>
 __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvParams<T> P) {
   // EHYB_MODE_*: STRICT and DEFAULT round every slice product and add
   // separately (reference order); they differ only in the long-row path
@@ -1096,10 +1096,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
   for (int it = 0, part = cta; part < P.n_parts; ++it, part += gridDim.x) {
   // unit `part` = chunks [c0, c0 + n_chunks) of partition q; row0 is the
   // unit's first row, the window is the whole partition's
-  const int64_t q = part / P.split;
-  const int64_t c0 = int64_t(part - q * P.split) * P.unit_chunks;
-  const int64_t n_chunks = (part_chunks - c0 < P.unit_chunks ? part_chunks - c0 : P.unit_chunks);
-  const int64_t unit_rows = (P.vec - c0 * 32 < n_chunks * 32 ? P.vec - c0 * 32 : n_chunks * 32);
+  // (SPLIT: compiled only into the variant launched when split > 1)
+  const int64_t q = SPLIT ? part / P.split : part;
+  const int64_t c0 = SPLIT ? int64_t(part - q * P.split) * P.unit_chunks : 0;
+  const int64_t n_chunks =
+      SPLIT ? (part_chunks - c0 < P.unit_chunks ? part_chunks - c0 : P.unit_chunks) : part_chunks;
+  const int64_t unit_rows =
+      SPLIT ? (P.vec - c0 * 32 < n_chunks * 32 ? P.vec - c0 * 32 : n_chunks * 32) : P.vec;
   const int64_t row0 = q * P.vec + c0 * 32;
   const T* xwin = P.x + q * P.vec;
   const int64_t s0 = P.er_sel == 2 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part);
@@ -1391,10 +1394,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
     // pooled slices of every partition, hidden behind the other warps' ELL
     // stream; with several partitions per CTA, the group whose owners ran in
     // the previous iteration
-    if (!persistent) pool_drain<T, STRICT>(P, lane, 0, ep);
+    if (!persistent) pool_drain<T, STRICT, SPLIT>(P, lane, 0, ep);
     else if (P.part_flag) {
-      pool_drain_group<T, STRICT>(P, lane, ep, it - 1);
-      if (P.pool_last_scratch && it == P.pool_groups - 1) pool_scratch_group<T, STRICT>(P, lane, ep, it);
+      pool_drain_group<T, STRICT, SPLIT>(P, lane, ep, it - 1);
+      if (P.pool_last_scratch && it == P.pool_groups - 1) pool_scratch_group<T, STRICT, SPLIT>(P, lane, ep, it);
     }
   }
   const int64_t st_lo = RING ? int64_t(__ldg(P.part_stage_ptr + part)) : 0;
@@ -1547,7 +1550,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
         atomicMax(P.timing + 8 * cta + i, globaltimer());
     };
     stamp(4);
-    if (!persistent) pool_drain<T, STRICT>(P, lane, 0, ep);  // whatever the ER-first warps left
+    if (!persistent) pool_drain<T, STRICT, SPLIT>(P, lane, 0, ep);  // whatever the ER-first warps left
     // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
     for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
       while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
@@ -1598,10 +1601,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       st_release_gpu(P.part_flag + last, ep);
     }
     const int g_end = P.pool_last_scratch ? P.pool_groups - 1 : P.pool_groups;
-    for (int g = 0; g < g_end; ++g) pool_drain_group<T, STRICT>(P, lane, ep, g);
+    for (int g = 0; g < g_end; ++g) pool_drain_group<T, STRICT, SPLIT>(P, lane, ep, g);
     if (P.pool_last_scratch) {
       const int gl = P.pool_groups - 1;
-      pool_scratch_group<T, STRICT>(P, lane, ep, gl);
+      pool_scratch_group<T, STRICT, SPLIT>(P, lane, ep, gl);
       const int pl = cta + gl * int(gridDim.x);  // this CTA's partition in the last group
       if (pl < P.n_parts) {
         const int32_t q0 = __ldg(P.pool_own_ptr + pl), q1 = __ldg(P.pool_own_ptr + pl + 1);
@@ -1622,7 +1625,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvPa
       }
     }
   } else if (persistent && P.do_er && P.pool_own_ptr) {
-    pool_drain<T, STRICT>(P, lane, 0, ep);
+    pool_drain<T, STRICT, SPLIT>(P, lane, 0, ep);
     __syncthreads();
     for (int64_t t = claim(&next_pcomb);; t = claim(&next_pcomb)) {
       int64_t base = 0;
