@@ -121,6 +121,36 @@ EHYB_API int ehyb_assemble(int64_t n, int64_t nnz, const int64_t* rows, const in
                            int64_t* out_slots_ell, void** out_val_er, uint32_t** out_col_er,
                            int64_t* out_slots_er);
 
+/* ---------------------------------------------- GPU preprocessing
+ * The same results as ehyb_build_graph / ehyb_classify_rows /
+ * ehyb_build_reorder_plan / ehyb_assemble (bit-exact), computed on a GPU:
+ * the COO is uploaded once (ehyb_gprep_create; entries grouped by row,
+ * column and entry index with a stable radix sort), build_graph returns the
+ * adjacency like ehyb_build_graph, assemble takes the (host-computed)
+ * partition and fills the outputs of the three host calls at once.
+ * Caller-alloc: inner/outer/row_order/arrange i64[n], reorder/inverse
+ * i64[padded], position_ell i32[padded/warp+1], width_ell i32[padded/warp],
+ * ell_row_widths i32[padded], part_boundary i32[n_parts+1]. Lib-alloc
+ * (ehyb_free): er_row_order, y_idx_er i64[n_er], position_er i32[n_er_sl+1],
+ * width_er i32[n_er_sl], er_row_widths i32[n_er], the four slab arrays. */
+typedef struct ehyb_gprep ehyb_gprep;
+EHYB_API int ehyb_gprep_create(int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                               const double* values, int device, ehyb_gprep** out);
+EHYB_API int ehyb_gprep_destroy(ehyb_gprep* c);
+EHYB_API int ehyb_gprep_build_graph(ehyb_gprep* c, int64_t* adj_ptr, int32_t** out_adj,
+                                    int64_t* out_n_adj);
+EHYB_API int ehyb_gprep_assemble(ehyb_gprep* c, const int64_t* assignment, int64_t n_parts,
+                                 int64_t vec, int64_t warp, int32_t tau,
+                                 int64_t* inner, int64_t* outer, int64_t* row_order,
+                                 int64_t** out_er_row_order, int64_t* out_n_er,
+                                 int64_t* reorder, int64_t* inverse, int64_t* arrange,
+                                 int64_t** out_y_idx_er,
+                                 int32_t* position_ell, int32_t* width_ell, int32_t* ell_row_widths,
+                                 int32_t* part_boundary, int32_t** out_position_er,
+                                 int32_t** out_width_er, int32_t** out_er_row_widths,
+                                 void** out_val_ell, uint16_t** out_col_ell, int64_t* out_slots_ell,
+                                 void** out_val_er, uint32_t** out_col_er, int64_t* out_slots_er);
+
 /* Host view of an assembled EhybMatrix (format.py:202-248). Array lengths
  * travel beside their pointers so ehyb_check can validate them. */
 typedef struct ehyb_host_matrix {

@@ -104,6 +104,16 @@ _PROTOS = {
                                 i32p, i32p, i32p, i32p, i32p, i32p, i32p,
                                 C.POINTER(vp), C.POINTER(u16p), i64p, C.POINTER(vp),
                                 C.POINTER(u32p), i64p]),
+    "ehyb_gprep_create": (C.c_int, [C.c_int64, C.c_int64, i64p, i64p, f64p, C.c_int,
+                                    C.POINTER(vp)]),
+    "ehyb_gprep_destroy": (C.c_int, [vp]),
+    "ehyb_gprep_build_graph": (C.c_int, [vp, i64p, C.POINTER(i32p), i64p]),
+    "ehyb_gprep_assemble": (C.c_int, [vp, i64p, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                      i64p, i64p, i64p, C.POINTER(i64p), i64p,
+                                      i64p, i64p, i64p, C.POINTER(i64p),
+                                      i32p, i32p, i32p, i32p, C.POINTER(i32p), C.POINTER(i32p),
+                                      C.POINTER(i32p), C.POINTER(vp), C.POINTER(u16p), i64p,
+                                      C.POINTER(vp), C.POINTER(u32p), i64p]),
     "ehyb_check": (C.c_int, [C.POINTER(HostMatrix)]),
     "ehyb_dev_create": (C.c_int, [C.POINTER(HostMatrix), C.c_int, C.POINTER(vp)]),
     "ehyb_dev_create_shard": (C.c_int, [C.POINTER(HostMatrix), C.POINTER(ShardPlan), C.c_int,

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libehyb_b200.so")
 
-SOURCES = ["prep_common.cpp", "prep.cpp", "device.cu"]
+SOURCES = ["prep_common.cpp", "prep.cpp", "device.cu", "prep_gpu.cu"]
 HEADERS = ["ehyb_common.h", "kernels.cuh", os.path.join("..", "..", "include", "ehyb_b200.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

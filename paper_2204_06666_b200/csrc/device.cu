@@ -530,8 +530,13 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   // default: fp32 slabs interleaved (4-byte values and 2-byte columns fetch 128 /
   // 64 B per warp instruction in the SELL layout, below the rate the HBM
   // stream needs: profiles/stream_probe_r2.txt; cfg3 fp32 114.9 vs 119.2 us),
-  // fp64 in the reference's SELL layout (cfg2 equal, cfg5 992 vs 1031 us)
-  h->ell_vec = C == 32 && env_double("EHYB_VEC", tb == 4 ? 1.0 : 0.0) != 0.0 &&
+  // fp64 interleaved when one wave of CTAs covers the partitions (cfg2 104.3
+  // vs 106.5 us) and in the reference's SELL layout for persistent CTAs (cfg5
+  // 963 vs 990 us)
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const bool one_wave = (p1 - p0) <= int64_t(sms);  // one CTA per SM covers every partition
+  h->ell_vec = C == 32 && env_double("EHYB_VEC", (tb == 4 || one_wave) ? 1.0 : 0.0) != 0.0 &&
                env_double("EHYB_RING", 0.0) == 0.0;
   if (h->ell_vec) {
     std::vector<char> pv(size_t(std::max<int64_t>(slots, 1)) * tb);
@@ -634,7 +639,7 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->smem = h->win_bytes + size_t(h->er_buf_slices) * 32 * buf_slot;
   const int64_t chunks = (vec + 31) / 32;
   // one warp per chunk up to 1024 threads, plus the ring producer warp
-  h->threads = int(std::min<int64_t>(kMaxThreads, std::max<int64_t>(64, chunks * 32 + 32)));
+  h->threads = int(std::min<int64_t>(max_threads_for(int(tb)), std::max<int64_t>(64, chunks * 32 + 32)));
   int per_sm = 0;
   CUDA_TRY(occupancy(h.get(), &per_sm));
   h->max_ctas = std::max<int64_t>(1, int64_t(per_sm) * h->sm_count);
@@ -1098,8 +1103,9 @@ EHYB_API int ehyb_dev_tune(ehyb_dev* h, int key, int64_t value) {
     case EHYB_TUNE_PREFETCH_ELL: h->pf_ell = int(std::max<int64_t>(0, value)); return 0;
     case EHYB_TUNE_PREFETCH_ER: h->pf_er = value ? 1 : 0; return 0;
     case EHYB_TUNE_THREADS:
-      if (value < 32 || value > kMaxThreads || value % 32)
-        return fail("threads must be a multiple of 32 in [32, " + std::to_string(kMaxThreads) + "]");
+      if (value < 32 || value > max_threads_for(h->tau) || value % 32)
+        return fail("threads must be a multiple of 32 in [32, " +
+                    std::to_string(max_threads_for(h->tau)) + "]");
       h->threads = int(value);
       return 0;
     case EHYB_TUNE_ER_WARPS: h->er_warps = int(std::max<int64_t>(0, value)); return 0;

@@ -31,10 +31,19 @@ constexpr int kUnroll = 8;        // slots per lane in flight
 #ifndef EHYB_POOL_BATCH_F64
 #define EHYB_POOL_BATCH_F64 1
 #endif
-#ifndef EHYB_MAX_THREADS
-#define EHYB_MAX_THREADS 1024
+// fused-kernel CTA size cap per value type = its register budget (one CTA per
+// SM): fp32 1024 threads x 64 registers, fp64 768 x 80 (the fp64 kernel
+// wants ~78 registers; at 64 it spills, and the persistent K > 1 path runs
+// 3% faster with the fatter warps: DESIGN.md §8)
+#ifndef EHYB_MAX_THREADS_F32
+#define EHYB_MAX_THREADS_F32 1024
 #endif
-constexpr int kMaxThreads = EHYB_MAX_THREADS;  // fused kernel CTA size cap (register budget)
+#ifndef EHYB_MAX_THREADS_F64
+#define EHYB_MAX_THREADS_F64 768
+#endif
+constexpr int max_threads_for(int tau) { return tau == 4 ? EHYB_MAX_THREADS_F32 : EHYB_MAX_THREADS_F64; }
+constexpr int kMaxThreads = EHYB_MAX_THREADS_F32 > EHYB_MAX_THREADS_F64 ? EHYB_MAX_THREADS_F32
+                                                                        : EHYB_MAX_THREADS_F64;
 constexpr int kTmaChunk = 32768;  // bytes per cp.async.bulk instruction
 
 template <typename T>
@@ -1028,7 +1037,8 @@ constexpr int kMaxErBuf = 2048;                        // buffered own ER slices
 // ER row whose ELL chunk is still in flight waits on that chunk's done bit,
 // so y[r] = y_ell[r] + er_acc keeps the reference's order of operations.
 template <typename T, int MODE, bool C32, bool SMEM, bool RING, bool P2P = false, bool SPLIT = false>
-__global__ void __launch_bounds__(kMaxThreads, 1) spmv_fused_kernel(const SpmvParams<T> P) {
+__global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
+    spmv_fused_kernel(const SpmvParams<T> P) {
   // EHYB_MODE_*: STRICT and DEFAULT round every slice product and add
   // separately (reference order); they differ only in the long-row path
   constexpr bool STRICT = MODE != EHYB_MODE_FMA;

@@ -709,7 +709,9 @@ def bench_main(args, clock_cls=None):
         m = CooMatrix(n, n, r, c, v)
         nnz = m.nnz
         del r, c, v
-        e = build_ehyb(m, tau=tau, profile=prof)
+        from .gpu_prep import build_ehyb_gpu
+
+        e = build_ehyb_gpu(m, tau=tau, profile=prof, device=local)
         del m
         if world > 1 and name != "weak":
             single = single_gpu_reference(e, local, args)

@@ -114,7 +114,7 @@ def main():
     pfrl = [int(v) for v in args.pf_er.split(",")]
     for (pool, ercost, ring, skb, vec), h in handles.items():
         for pfer, ew, ah, pfe in itertools.product(pfrl, ewl, ahl, pfl):
-            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=int(os.environ.get('EHYB_THREADS', '1024')), er_warps=ew, claim_ahead=ah)
+            h.tune(prefetch_ell=pfe, prefetch_er=pfer, threads=int(os.environ.get('EHYB_THREADS', h.info()['threads_per_cta'])), er_warps=ew, claim_ahead=ah)
             us = time_variant(h, xr, y, args.reps, stream)
             ok = gold is None or digest(y.cpu().numpy()) == gold["y_reordered"]
             results.append(dict(pool=pool, er_cost=ercost, ring=ring, stage_kb=skb, vec=vec,
@@ -129,7 +129,7 @@ def main():
             print(json.dumps(results[-1]), flush=True)
     best = min(results, key=lambda r: r["us"])
     dm = handles[(best["pool"], best["er_cost"], best["ring"], best["stage_kb"], best["vec"])]
-    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=int(os.environ.get('EHYB_THREADS', '1024')),
+    dm.tune(prefetch_ell=best["pf_ell"], prefetch_er=best["pf_er"], threads=int(os.environ.get('EHYB_THREADS', dm.info()['threads_per_cta'])),
             er_warps=best["er_warps"], claim_ahead=best["ahead"])
     prof = cta_profile(dm, xr, y, stream, n_ctas)
     # the two phases on their own (split launches): what each costs in isolation
