@@ -1,0 +1,14 @@
+#!/bin/bash
+TAG=${1:-epi2}
+OUT=gpurun_out; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+S=scripts/kernel_sweep.py
+for EPI in 1 0; do
+for C in cfg2 cfg3f64 cfg5 cfg3f32; do
+  AH=3; [ $C = cfg3f32 ] && AH=0
+  V=0; [ $C = cfg3f32 ] && V=1; [ $C = cfg2 ] && V=1
+  EHYB_EPI_COMBINE=$EPI timeout 900 python $S --config $C --pool 0.95 --er-cost 5.0 --er-warps 8 --pf-ell 0 --pf-er 1 --reps 300 --vec $V --ahead $AH > $OUT/exp_${TAG}_e${EPI}_$C.jsonl 2> $OUT/exp_${TAG}_e${EPI}_$C.err
+  echo "epi $EPI $C rc=$?" >> $OUT/exp_${TAG}_summary.txt
+done; done
+timeout 1800 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> $OUT/exp_${TAG}_summary.txt
+cat $OUT/exp_${TAG}_summary.txt; tail -3 $OUT/pytest_gpu_$TAG.log
