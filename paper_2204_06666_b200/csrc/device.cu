@@ -691,10 +691,10 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   const bool small = chunks <= 2 * int64_t(h->threads / 32);
   if (tb == 4) h->ell_ahead = h->er_ahead = 0;  // fp32: measured 1.5% better without
   if (small) {
-    h->er_warps = 16;
+    h->er_warps = h->threads / 64;  // half the warps (16 of 32 at 1024 threads)
     h->ell_ahead = h->er_ahead = 0;
   }
-  const double pool_factor = env_double("EHYB_POOL_FACTOR", small ? 1e30 : 0.95);
+  const double pool_factor = env_double("EHYB_POOL_FACTOR", small ? 1e30 : 0.9);
   const double er_cost = env_double("EHYB_ER_COST", 5.0);
   std::vector<double> ell_cost(static_cast<size_t>(n_units)), er_total(static_cast<size_t>(n_units), 0.0);
   double total = 0.0;
