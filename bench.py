@@ -115,8 +115,26 @@ def build_workload(name: str):
     del r, c, v
     prof = W.CONFIG_PROFILES.get(name)
     params = E.compute_params(n, tau, E.DeviceProfile(*prof) if prof else E.B200_PROFILE)
+    if os.environ.get("EHYB_BENCH_PREP", "gpu") == "host":  # e.g. launch lists: no prep kernels
+        t0 = time.perf_counter()
+        g = E.build_graph(m)
+        tg = time.perf_counter()
+        parts = E.partition_graph(g, params.n_parts, params.vec_cache_size, seed=0)
+        t1 = time.perf_counter()
+        cls = E.classify_rows(m, parts)
+        plan = E.build_reorder_plan(cls, params, parts)
+        e = E.assemble_ehyb(m, plan, params, parts)
+        t2 = time.perf_counter()
+        return m, e, dict(generate_s=t_gen, partition_s=t1 - t0, reorder_assemble_s=t2 - t1,
+                          build_graph_s=tg - t0, partition_graph_s=t1 - tg, where="host")
     # GPU preprocessing (build_graph, classify / reorder / assemble on the
-    # device, the BFS partitioner on the host); byte-identical to the host path
+    # device, the BFS partitioner on the host); byte-identical to the host path.
+    # A tiny matrix first loads the preprocessing kernels' modules (a one-time
+    # per-process cost of CUDA lazy loading, ~0.4 s), so the timing below is
+    # the steady-state pipeline
+    nw, rw, cw, vw = W.stencil27(8, 8, 8)
+    E.build_ehyb_gpu(E.CooMatrix(nw, nw, rw, cw, vw), tau=tau, profile=E.DeviceProfile(4, 32, 8192),
+                     device=0)
     t = {}
     t0 = time.perf_counter()
     e = E.build_ehyb_gpu(m, tau=tau, profile=E.DeviceProfile(*prof) if prof else E.B200_PROFILE,
@@ -128,7 +146,8 @@ def build_workload(name: str):
                       reorder_assemble_s=t["reorder_assemble_s"], upload_s=t["upload_s"],
                       build_graph_s=t["build_graph_s"], partition_graph_s=t["partition_graph_s"],
                       total_s=total, where="GPU (build_graph, classify/reorder/assemble) + host "
-                                           "(BFS partition_graph)")
+                                           "(BFS partition_graph); kernel modules loaded "
+                                           "beforehand (one-time lazy-loading cost excluded)")
 
 
 def golden_y_digest(name: str):

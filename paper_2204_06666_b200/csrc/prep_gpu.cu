@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -87,20 +88,28 @@ struct DevBuf {
 // double-buffered pinned staging area: the host side of every chunk is
 // copied by all OpenMP threads (which also spreads the first-touch page
 // faults of fresh output arrays), overlapped with the DMA of the other half.
+// the pinned area is process-wide (page-locking 64 MB costs 100+ ms); one
+// preprocessing context uses it at a time
+std::mutex g_pinned_mu;
+unsigned char* g_pinned = nullptr;
+
 struct Staging {
   static constexpr size_t kHalf = size_t(32) << 20;
   unsigned char* buf = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::unique_lock<std::mutex> hold;
   ~Staging() {
-    if (buf) cudaFreeHost(buf);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
   cudaError_t init() {
     if (buf) return cudaSuccess;
-    cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&buf), 2 * kHalf);
+    hold = std::unique_lock<std::mutex>(g_pinned_mu);
+    cudaError_t e = cudaSuccess;
+    if (!g_pinned) e = cudaMallocHost(reinterpret_cast<void**>(&g_pinned), 2 * kHalf);
+    buf = g_pinned;
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
     return e;
@@ -115,6 +124,7 @@ struct Staging {
     }
   }
   cudaError_t h2d(void* dev, const void* host, size_t bytes) {
+    if (bytes <= kHalf) return cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice);
     cudaError_t e = init();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();  // earlier default-stream work is done
     for (size_t off = 0, i = 0; e == cudaSuccess && off < bytes; off += kHalf, ++i) {
@@ -130,6 +140,7 @@ struct Staging {
     return e;
   }
   cudaError_t d2h(void* host, const void* dev, size_t bytes) {
+    if (bytes <= kHalf) return bytes ? cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost) : cudaSuccess;
     cudaError_t e = init();
     if (e != cudaSuccess || bytes == 0) return e;
     e = cudaDeviceSynchronize();  // results of the default-stream kernels
@@ -455,8 +466,7 @@ EHYB_API int ehyb_gprep_create(int64_t n, int64_t nnz, const int64_t* rows, cons
     GP_TRY(rd.alloc(size_t(nnz) * 8));
     GP_TRY(cd.alloc(size_t(nnz) * 8));
     GP_TRY(vd.alloc(size_t(nnz) * 8));
-    GP_TRY(c->stage.init());
-    st.mark("create: device + pinned alloc");
+    st.mark("create: device alloc");
     if (nnz) {
       GP_TRY(c->stage.h2d(rd.p, rows, size_t(nnz) * 8));
       GP_TRY(c->stage.h2d(cd.p, cols, size_t(nnz) * 8));

@@ -20,5 +20,5 @@ for C in cfg2 cfg3f32; do
   ncu -i $OUT/prof_${TAG}_${C}_er.ncu-rep --page raw --csv > $OUT/prof_${TAG}_${C}_er.raw.csv 2>/dev/null
   rm -f $OUT/prof_${TAG}_${C}_er.ncu-rep
 done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_${TAG}_cfg2.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-cusparse > /dev/null 2> $OUT/ncu_launch_$TAG.err; echo "launches rc=$?" >> $OUT/ncu_${TAG}_summary.txt
+EHYB_BENCH_PREP=host timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_${TAG}_cfg2.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-cusparse > /dev/null 2> $OUT/ncu_launch_$TAG.err; echo "launches rc=$?" >> $OUT/ncu_${TAG}_summary.txt
 du -sh $OUT; cat $OUT/ncu_${TAG}_summary.txt

@@ -13,7 +13,13 @@ from paper_2204_06666_b200 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
+ap.add_argument("--torch", action="store_true", help="initialise torch's CUDA context first (as bench.py)")
 args = ap.parse_args()
+if args.torch:
+    import torch
+
+    torch.cuda.set_device(0)
+    torch.zeros(1, device="cuda:0")
 n, r, c, v, tau = W.build_config(args.config)
 m = E.CooMatrix(n, n, r, c, v)
 prof = W.CONFIG_PROFILES.get(args.config)
@@ -30,6 +36,8 @@ for it in range(2):
     t = {}
     t0 = time.perf_counter()
     e2 = E.build_ehyb_gpu(m, tau=tau, profile=prof, device=0, timings=t)
+    import sys as _s
+    print("gpu done", flush=True, file=_s.stderr)
     print("gpu:", {k: round(x, 3) for k, x in t.items()}, f"total {time.perf_counter()-t0:.3f} s",
           flush=True)
     del e, e2
