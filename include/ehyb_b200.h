@@ -226,7 +226,7 @@ EHYB_API int ehyb_dev_info_get(const ehyb_dev* h, ehyb_dev_info* out);
 #define EHYB_TUNE_PREFETCH_ER 2
 #define EHYB_TUNE_THREADS 3
 #define EHYB_TUNE_TIMING 4
-#define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 4) */
+#define EHYB_TUNE_ER_WARPS 5 /* warps that compute own ER rows before ELL (default 6; half the CTA for small partitions) */
 #define EHYB_TUNE_CLAIM_AHEAD 6 /* bit0: ELL chunks, bit1: ER slices claimed one ahead */
 #define EHYB_TUNE_PHASES 7      /* measurement only: bit0 skips the ER work, bit1 the ELL
                                    stream (y is then incomplete) */

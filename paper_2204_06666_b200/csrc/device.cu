@@ -136,7 +136,7 @@ struct ehyb_dev {
   unsigned int* pool_ctr = nullptr;
   unsigned int* epoch_dev = nullptr;  // [2] launch epoch, CTAs finished (device-side: graph-safe)
   // own-ER shared-memory buffer
-  int er_buf_slices = 0, er_buf_offset = 0, er_warps = 8;
+  int er_buf_slices = 0, er_buf_offset = 0, er_warps = 6;  // measured best: cfg2 102.5 vs 103.7 us at 8
   size_t ring_offset = 0, ring_bytes = 0;  // ELL staging ring (0 = register path)
   int ring_stages = 0, stage_bytes = 0, stage_vbytes = 0;
   bool ell_vec = false;  // ELL slices in the 128-bit interleaved layout
