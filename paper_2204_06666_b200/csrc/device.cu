@@ -117,6 +117,8 @@ struct ehyb_dev {
   int32_t* pool_own_ptr = nullptr;
   int32_t* pool_own_idx = nullptr;
   void* pool_acc = nullptr;
+  int32_t* pool_pos = nullptr;   // owner-major position of each pooled slice
+  int32_t* pool_rows = nullptr;  // pooled slices' rows, owner-major
   void* own_acc = nullptr;  // own ER sums beyond the shared-memory buffer
   // P2P halo exchange (shards): x_ext and flags owned by the handle (IPC-able),
   // the pull plan and the peers' mapped buffers
@@ -181,7 +183,7 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, own_acc, p2p_x, p2p_flags, pull_src, pull_off, peer_x_dev, peer_flags_dev,
+                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_pos, pool_rows, own_acc, p2p_x, p2p_flags, pull_src, pull_off, peer_x_dev, peer_flags_dev,
                     pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
@@ -241,6 +243,8 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.pool_own_ptr = h->pool_own_ptr;
   P.pool_own_idx = h->pool_own_idx;
   P.pool_acc = static_cast<T*>(h->pool_acc);
+  P.pool_pos = h->pool_pos;
+  P.pool_rows = h->pool_rows;
   P.own_acc = static_cast<T*>(h->own_acc);
   P.n_halo = h->n_halo;
   P.local_rows = h->local_rows;
@@ -1043,6 +1047,18 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
       oidx[size_t(fill[size_t(order[size_t(sl)].q)]++)] = int32_t(sl);
     CUDA_TRY(upload(&h->pool_own_ptr, optr.data(), optr.size() * 4, &h->bytes));
     CUDA_TRY(upload(&h->pool_own_idx, oidx.data(), oidx.size() * 4, &h->bytes));
+    // owner-major scratch: pooled slice s writes its sums at position pos[s]
+    // of its owner's list; the owner reads rows and sums contiguously
+    {
+      std::vector<int32_t> ppos(oidx.size()), prow(oidx.size() * 32);
+      for (size_t i = 0; i < oidx.size(); ++i) {
+        const int64_t sl = oidx[i];
+        ppos[size_t(sl - h->pool_lo)] = int32_t(i);
+        std::memcpy(&prow[i * 32], &erows[size_t(sl) * 32], 32 * 4);
+      }
+      CUDA_TRY(upload(&h->pool_pos, ppos.data(), ppos.size() * 4, &h->bytes));
+      CUDA_TRY(upload(&h->pool_rows, prow.data(), prow.size() * 4, &h->bytes));
+    }
     const size_t acc_bytes = size_t(h->pool_hi - h->pool_lo) * 32 * tb;
     CUDA_TRY(cudaMalloc(&h->pool_acc, acc_bytes));
     CUDA_TRY(cudaMalloc(&h->pool_done, size_t(n_units) * 8 + 16));

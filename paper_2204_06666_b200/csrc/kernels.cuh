@@ -85,7 +85,9 @@ struct SpmvParams {
   unsigned int* pool_done;          // [2][n_parts] computed pooled slices per owner, by epoch
   const int32_t* __restrict__ pool_own_ptr;  // [n_parts+1] pooled slices of each partition
   const int32_t* __restrict__ pool_own_idx;  // their slice indices
-  T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums
+  T* pool_acc;                      // [(pool_hi-pool_lo)*32] pooled row sums, owner-major order
+  const int32_t* __restrict__ pool_pos;   // [pool slices] owner-major position of each pooled slice
+  const int32_t* __restrict__ pool_rows;  // [pool slices*32] their rows, owner-major order
   T* own_acc;                       // [er_slices*32] own ER row sums beyond the smem buffer (or null)
   // P2P halo (shards, exchange = peer memory): the launch itself pulls the
   // halo from the peers' x buffers over NVLink and finishes halo rows once
@@ -847,8 +849,9 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     n_pend = 0;
   };
   auto finish = [&](int64_t s, const ErMeta& m) {
+    const int64_t pp = __ldg(P.pool_pos + (s - P.pool_lo));  // in flight with the slice
     const T acc = er_slice_compute<T, STRICT>(P, m);
-    P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc;
+    P.pool_acc[pp * 32 + lane] = acc;
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
     const uint32_t owner = unit_of_row<SPLIT>(P, uint32_t(rw0 & kRowMask));
     if (n_pend == 0) pend0 = owner;
@@ -878,10 +881,12 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     const bool two = s + 1 < P.pool_hi;
     const ErMeta ma = er_claimed_meta(P, s, P.pool_hi, lane);
     const ErMeta mb = er_claimed_meta(P, s + 1, P.pool_hi, lane);
+    const int64_t pa = __ldg(P.pool_pos + (s - P.pool_lo));
+    const int64_t pb = two ? __ldg(P.pool_pos + (s + 1 - P.pool_lo)) : 0;
     T acc_a, acc_b;
     er_pair_compute<T, STRICT>(P, ma, mb, acc_a, acc_b);
-    P.pool_acc[(s - P.pool_lo) * 32 + lane] = acc_a;
-    if (two) P.pool_acc[(s + 1 - P.pool_lo) * 32 + lane] = acc_b;
+    P.pool_acc[pa * 32 + lane] = acc_a;
+    if (two) P.pool_acc[pb * 32 + lane] = acc_b;
     __threadfence();
     __syncwarp();
     const int32_t ra = __shfl_sync(0xffffffffu, ma.rw, 0), rb = __shfl_sync(0xffffffffu, mb.rw, 0);
@@ -962,7 +967,8 @@ __device__ void pool_scratch_group(const SpmvParams<T>& P, int lane, uint32_t ep
     const int64_t s = lo + int64_t(__shfl_sync(0xffffffffu, v, 0));
     if (s >= hi) break;
     const ErMeta m = er_claimed_meta(P, s, hi, lane);
-    P.pool_acc[(s - P.pool_lo) * 32 + lane] = er_slice_compute<T, STRICT>(P, m);
+    const int64_t pp = __ldg(P.pool_pos + (s - P.pool_lo));
+    P.pool_acc[pp * 32 + lane] = er_slice_compute<T, STRICT>(P, m);
     const int32_t rw0 = __shfl_sync(0xffffffffu, m.rw, 0);  // lane 0 always holds a row
     __threadfence();
     __syncwarp();
@@ -1585,13 +1591,15 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
       // every pooled slice is claimed by now (this warp drained the pool
       // above), so only slices still in flight elsewhere remain
       while (ld_acquire_gpu(done) != unsigned(q1 - q0)) __nanosleep(128);
+      // owner-major scratch: the row and its sum in one round trip
       for (int64_t idx = claim(&next_pcomb); idx < q1 - q0; idx = claim(&next_pcomb)) {
-        const int64_t sl = __ldg(P.pool_own_idx + q0 + idx);
-        const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
+        const int64_t o = (q0 + idx) * 32 + lane;
+        const int32_t rw = __ldg(P.pool_rows + o);
+        const T acc = __ldcg(P.pool_acc + o);
         if (rw >= 0) {
           const int64_t r = rw & kRowMask;
           wait_chunk(r);
-          P.y[r] = add_rn(__ldcg(P.y + r), __ldcg(P.pool_acc + (sl - P.pool_lo) * 32 + lane));
+          P.y[r] = add_rn(__ldcg(P.y + r), acc);
         }
       }
     }
@@ -1624,11 +1632,12 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
             while (ld_acquire_gpu(done) != unsigned(q1 - q0)) __nanosleep(64);
           __syncwarp();
           for (int64_t t = wid; t < q1 - q0; t += int64_t(blockDim.x >> 5)) {
-            const int64_t sl = __ldg(P.pool_own_idx + q0 + t);
-            const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
+            const int64_t o = (q0 + t) * 32 + lane;
+            const int32_t rw = __ldg(P.pool_rows + o);
+            const T acc = __ldcg(P.pool_acc + o);
             if (rw >= 0) {
               const int64_t r = rw & kRowMask;
-              P.y[r] = add_rn(__ldcg(P.y + r), __ldcg(P.pool_acc + (sl - P.pool_lo) * 32 + lane));
+              P.y[r] = add_rn(__ldcg(P.y + r), acc);
             }
           }
         }
@@ -1653,11 +1662,12 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
       if (pt < 0) break;
       const unsigned int* done = P.pool_done + (ep & 1u) * uint32_t(P.n_parts) + uint32_t(pt);
       while (ld_acquire_gpu(done) != unsigned(cnt)) __nanosleep(128);
-      const int64_t sl = __ldg(P.pool_own_idx + q0 + (t - base));
-      const int32_t rw = __ldg(P.er_rows + sl * 32 + lane);
+      const int64_t o = (q0 + (t - base)) * 32 + lane;
+      const int32_t rw = __ldg(P.pool_rows + o);
+      const T acc = __ldcg(P.pool_acc + o);
       if (rw >= 0) {
         const int64_t r = rw & kRowMask;
-        P.y[r] = add_rn(__ldcg(P.y + r), __ldcg(P.pool_acc + (sl - P.pool_lo) * 32 + lane));
+        P.y[r] = add_rn(__ldcg(P.y + r), acc);
       }
     }
   }
