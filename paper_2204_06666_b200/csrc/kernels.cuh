@@ -1567,18 +1567,38 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
     };
     stamp(4);
     if (!persistent) pool_drain<T, STRICT, SPLIT>(P, lane, 0, ep);  // whatever the ER-first warps left
-    // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc
-    for (int64_t idx = claim(&next_comb); idx < n_buf; idx = claim(&next_comb)) {
+    // combine the buffered own ER rows: y[r] = y_ell[r] + er_acc, two
+    // slices per claim so their row and y reads overlap
+    constexpr int kCs = sizeof(T) == 8 ? 2 : 1;  // fp32: one per claim (register budget)
+    for (;;) {
+      int v = 0;
+      if (lane == 0) v = atomicAdd(&next_comb, kCs);
+      const int64_t idx = __shfl_sync(0xffffffffu, v, 0);
+      if (idx >= n_buf) break;
+      const bool two = kCs == 2 && idx + 1 < n_buf;
+      const int32_t rw = __ldg(P.er_rows + (s0 + idx) * 32 + lane);
+      const int32_t rw2 = two ? __ldg(P.er_rows + (s0 + idx + 1) * 32 + lane) : -1;
       while (!lds_volatile(&er_done[idx >> 5], 1u << (idx & 31))) {
       }
+      if (two)
+        while (!lds_volatile(&er_done[(idx + 1) >> 5], 1u << ((idx + 1) & 31))) {
+        }
       __threadfence_block();
-      const int32_t rw = __ldg(P.er_rows + (s0 + idx) * 32 + lane);
+      T y1 = T(0), y2 = T(0);
       if (rw >= 0) {
-        const int64_t r = rw & kRowMask;
-        wait_chunk(r);
-        P.y[r] = add_rn(__ldcg(P.y + r), idx < P.er_buf_slices ? er_buf[idx * 32 + lane]
-                                                                : __ldcg(buf_at(idx)));
+        wait_chunk(rw & kRowMask);
+        y1 = __ldcg(P.y + (rw & kRowMask));
       }
+      if (rw2 >= 0) {
+        wait_chunk(rw2 & kRowMask);
+        y2 = __ldcg(P.y + (rw2 & kRowMask));
+      }
+      if (rw >= 0)
+        P.y[rw & kRowMask] = add_rn(y1, idx < P.er_buf_slices ? er_buf[idx * 32 + lane]
+                                                              : __ldcg(buf_at(idx)));
+      if (rw2 >= 0)
+        P.y[rw2 & kRowMask] = add_rn(y2, idx + 1 < P.er_buf_slices ? er_buf[(idx + 1) * 32 + lane]
+                                                                   : __ldcg(buf_at(idx + 1)));
     }
     stamp(5);
     // pooled slices of this partition: once all are in, y[r] = y_ell[r] + sum
@@ -1591,16 +1611,32 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
       // every pooled slice is claimed by now (this warp drained the pool
       // above), so only slices still in flight elsewhere remain
       while (ld_acquire_gpu(done) != unsigned(q1 - q0)) __nanosleep(128);
-      // owner-major scratch: the row and its sum in one round trip
-      for (int64_t idx = claim(&next_pcomb); idx < q1 - q0; idx = claim(&next_pcomb)) {
+      // owner-major scratch: the row and its sum in one round trip, two
+      // pooled slices per claim so their reads overlap
+      // (fp32 keeps one slice per claim: measured 111.9 vs 120.3 us on cfg3)
+      constexpr int kPs = sizeof(T) == 8 ? 2 : 1;
+      for (;;) {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&next_pcomb, kPs);
+        const int64_t idx = __shfl_sync(0xffffffffu, v, 0);
+        if (idx >= q1 - q0) break;
+        const bool two = kPs == 2 && idx + 1 < q1 - q0;
         const int64_t o = (q0 + idx) * 32 + lane;
         const int32_t rw = __ldg(P.pool_rows + o);
         const T acc = __ldcg(P.pool_acc + o);
+        const int32_t rw2 = two ? __ldg(P.pool_rows + o + 32) : -1;
+        const T acc2 = two ? __ldcg(P.pool_acc + o + 32) : T(0);
+        T y1 = T(0), y2 = T(0);
         if (rw >= 0) {
-          const int64_t r = rw & kRowMask;
-          wait_chunk(r);
-          P.y[r] = add_rn(__ldcg(P.y + r), acc);
+          wait_chunk(rw & kRowMask);
+          y1 = __ldcg(P.y + (rw & kRowMask));
         }
+        if (rw2 >= 0) {
+          wait_chunk(rw2 & kRowMask);
+          y2 = __ldcg(P.y + (rw2 & kRowMask));
+        }
+        if (rw >= 0) P.y[rw & kRowMask] = add_rn(y1, acc);
+        if (rw2 >= 0) P.y[rw2 & kRowMask] = add_rn(y2, acc2);
       }
     }
     stamp(6);
