@@ -148,6 +148,7 @@ struct ehyb_dev {
   int32_t* st_chunks = nullptr;
   uint2* ch_stage = nullptr;
   int ell_ahead = 1, er_ahead = 1;
+  int32_t meta_off = -1;  // chunk metadata in dynamic smem (byte offset), -1 = global loads
   int phase_skip = 0;
   int32_t split = 1, unit_chunks = 0;  // work units per partition, chunks per unit
   int64_t n_units = 0;                 // launch work units (partitions x split)  // EHYB_TUNE_PHASES (dev): bit 0 skips the ER work, bit 1 the ELL stream
@@ -268,6 +269,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.n_parts = int32_t(h->n_units);
   P.split = h->split;
   P.unit_chunks = h->unit_chunks;
+  P.meta_off = h->meta_off;
   P.ell_ahead = h->ell_ahead;
   P.er_ahead = h->er_ahead;
   P.long_bits = h->long_bits;
@@ -295,6 +297,18 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   // work-unit split (several CTAs per partition): its own variant, so the
   // one-unit-per-partition kernel keeps the register allocation it had
   const bool split = h->split > 1;
+#ifdef EHYB_DEV_ONE
+  // dev experiments (EHYB_NVCC_FLAGS=-DEHYB_DEV_ONE=<tau> -DEHYB_DEV_MODE=<m>):
+  // one kernel variant compiled, every other launch kind refused
+  if (!(do_ell && h->window_in_smem) || split || h->p2p_active || h->ring_bytes > 0 || !C32)
+    return cudaErrorNotSupported;
+  size_t smem = (do_ell && (do_er || h->meta_off >= 0)) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
+  void (*kern)(const SpmvParams<T>) = spmv_fused_kernel<T, MODE, true, true, false>;
+  P.ring_offset = 0;
+  P.ring_stages = P.stage_bytes = P.stage_vbytes = 0;
+  P.part_stage_ptr = P.st_pos = P.st_slots = P.st_chunks = nullptr;
+  P.ch_stage = nullptr;
+#else
   void (*kern)(const SpmvParams<T>) =
       (do_ell && h->window_in_smem)
           ? (split ? spmv_fused_kernel<T, MODE, C32, true, false, false, true>
@@ -303,7 +317,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
                    : spmv_fused_kernel<T, MODE, C32, false, false>);
   // dynamic smem: [window | own-ER buffer | ELL ring]; the buffer is only
   // used when one launch runs both phases, the ring by any ELL launch
-  size_t smem = (do_ell && do_er) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
+  size_t smem = (do_ell && (do_er || h->meta_off >= 0)) ? h->smem : (P.window_in_smem ? h->win_bytes : 0);
   P.ring_offset = 0;
   P.ring_stages = P.stage_bytes = P.stage_vbytes = 0;
   P.part_stage_ptr = P.st_pos = P.st_slots = P.st_chunks = nullptr;
@@ -328,6 +342,7 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
       kern = split ? spmv_fused_kernel<T, MODE, true, true, false, true, true>
                    : spmv_fused_kernel<T, MODE, true, true, false, true>;
   }
+#endif  // EHYB_DEV_ONE
   if (!(do_ell && do_er)) {
     P.er_buf_slices = 0;
   }
@@ -370,6 +385,12 @@ template <typename T>
 cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
                         cudaStream_t st) {
   const bool c32 = h->warp == 32;
+#ifdef EHYB_DEV_ONE
+  if constexpr (sizeof(T) == EHYB_DEV_ONE) {
+    if (mode == EHYB_DEV_MODE && c32) return launch_typed<T, EHYB_DEV_MODE, true>(h, x, y, ell, er, st);
+  }
+  return cudaErrorNotSupported;
+#else
   if (mode == EHYB_MODE_FMA)
     return c32 ? launch_typed<T, EHYB_MODE_FMA, true>(h, x, y, ell, er, st)
                : launch_typed<T, EHYB_MODE_FMA, false>(h, x, y, ell, er, st);
@@ -378,6 +399,7 @@ cudaError_t launch_mode(const ehyb_dev* h, const void* x, void* y, int mode, boo
                : launch_typed<T, EHYB_MODE_DEFAULT, false>(h, x, y, ell, er, st);
   return c32 ? launch_typed<T, EHYB_MODE_STRICT, true>(h, x, y, ell, er, st)
              : launch_typed<T, EHYB_MODE_STRICT, false>(h, x, y, ell, er, st);
+#endif
 }
 
 cudaError_t launch_spmv(ehyb_dev* h, const void* x, void* y, int mode, bool ell, bool er,
@@ -408,10 +430,15 @@ double env_double(const char* name, double dflt) {
 
 template <typename T, int MODE>
 const void* fused_variant(bool c32, bool smem) {
+#ifdef EHYB_DEV_ONE
+  if constexpr (sizeof(T) == EHYB_DEV_ONE) return (const void*)spmv_fused_kernel<T, EHYB_DEV_MODE, true, true, false>;
+  return nullptr;
+#else
   return c32 ? (smem ? (const void*)spmv_fused_kernel<T, MODE, true, true, false>
                      : (const void*)spmv_fused_kernel<T, MODE, true, false, false>)
              : (smem ? (const void*)spmv_fused_kernel<T, MODE, false, true, false>
                      : (const void*)spmv_fused_kernel<T, MODE, false, false, false>);
+#endif
 }
 
 // resident CTAs per SM of the fused kernel for this handle's configuration:
@@ -431,6 +458,7 @@ cudaError_t occupancy(const ehyb_dev* h, int* per_sm) {
   }
   *per_sm = 1 << 30;
   for (const void* k : ks) {
+    if (!k) continue;
     if (h->smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
       if (e != cudaSuccess) return e;
@@ -698,6 +726,11 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     h->er_warps = h->threads / 64;  // half the warps (16 of 32 at 1024 threads)
     h->ell_ahead = h->er_ahead = 0;
   }
+  if (const double a = env_double("EHYB_CLAIM_AHEAD", -1.0); a >= 0.0) {  // dev override
+    h->ell_ahead = int(a) & 1;
+    h->er_ahead = (int(a) >> 1) & 1;
+  }
+  h->pf_ell = int(env_double("EHYB_PF_ELL", double(h->pf_ell)));
   const double pool_factor = env_double("EHYB_POOL_FACTOR", small ? 1e30 : 0.9);
   const double er_cost = env_double("EHYB_ER_COST", 5.0);
   std::vector<double> ell_cost(static_cast<size_t>(n_units)), er_total(static_cast<size_t>(n_units), 0.0);
@@ -777,7 +810,11 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     // window, at least 2 chunks of the widest slice; the own-ER buffer gives
     // way so the ring keeps >= EHYB_RING_KB (default 64 KB)
     h->ring_bytes = 0;
+#ifdef EHYB_DEV_ONE
+    if (false) {
+#else
     if (C == 32 && h->window_tma && env_double("EHYB_RING", 0.0) != 0.0) {
+#endif
       cudaFuncAttributes fa{};
       if (tb == 4)
         CUDA_TRY(cudaFuncGetAttributes(&fa, spmv_fused_kernel<float, EHYB_MODE_STRICT, true, true, true>));
@@ -808,6 +845,24 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
           h->ring_bytes = size_t(ns * sb);
         }
         h->smem = h->win_bytes + size_t(buf);
+      }
+    }
+    // per-unit chunk metadata {pos, eff} in shared memory after the own-ER
+    // buffer (32-row slices, staged window, no ring) when it fits the
+    // per-CTA budget the grid was sized for
+    // measured (profiles/ab_meta_r3.jsonl): fp32 (no claim-ahead) 114.7 ->
+    // 112.7 us on cfg3; persistent fp64 180.0 -> 176.5 us on cfg3 fp64; the
+    // one-wave fp64 path already hides the metadata behind its claim-ahead
+    // (cfg2 100.5 vs 102.5 us with it), so it keeps the global loads
+    h->meta_off = -1;
+    const bool meta_default = tb == 4 || n_units > h->max_ctas;
+    if (C == 32 && h->window_in_smem && h->ring_bytes == 0 &&
+        env_double("EHYB_META_SMEM", meta_default ? 1.0 : 0.0) != 0.0) {
+      const size_t off = (h->smem + 15) / 16 * 16;
+      const size_t bytes = size_t(unit_chunks) * 8;
+      if (off + bytes + kStaticReserve <= size_t(optin)) {
+        h->meta_off = int32_t(off);
+        h->smem = off + bytes;
       }
     }
     if (h->ring_stages > 0) {

@@ -135,6 +135,9 @@ struct SpmvParams {
   const int32_t* __restrict__ st_slots;
   const int32_t* __restrict__ st_chunks;
   const uint2* __restrict__ ch_stage;          // [local_rows/32]
+  int32_t meta_off;                 // >= 0: byte offset in dynamic smem of the unit's chunk
+                                    // metadata {pos, eff} (loaded once per partition; the
+                                    // per-chunk claims then read shared memory), -1 = global
   int32_t ell_ahead;                // 1 = claim the next ELL chunk (and its metadata) one ahead
   int32_t er_ahead;                 // 1 = same for ER slices
   // long rows (derived at upload): rows whose ELL or ER width exceeds the long
@@ -183,6 +186,13 @@ constexpr int32_t kRowMask = 0x3fffffff;
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// one lane's shared-memory counter claim: a plain atom.shared (the compiler
+// turns atomicAdd under `lane == 0` into a warp-aggregated sequence)
+__device__ __forceinline__ int atom_add_shared(int* p, int v) {
+  int r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(v) : "memory");
+  return r;
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
@@ -1098,7 +1108,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
   const bool persistent = int(gridDim.x) < P.n_parts;
   auto claim = [&](int* ctr) -> int64_t {
     int v = 0;
-    if (lane == 0) v = atomicAdd(ctr, 1);
+    if (lane == 0) v = atom_add_shared(ctr, 1);
     return __shfl_sync(0xffffffffu, v, 0);
   };
   // ring producer state (lane 0 of the last warp), kept across partitions
@@ -1121,6 +1131,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
       SPLIT ? (P.vec - c0 * 32 < n_chunks * 32 ? P.vec - c0 * 32 : n_chunks * 32) : P.vec;
   const int64_t row0 = q * P.vec + c0 * 32;
   const T* xwin = P.x + q * P.vec;
+  T* const y_lane = P.y + row0 + lane;  // this lane's row of chunk 0 of the unit
   const int64_t s0 = P.er_sel == 2 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part);
   const int64_t s1 = P.er_sel == 1 ? __ldg(P.er_part_mid + part) : __ldg(P.er_part_ptr + part + 1);
   const uint32_t phase = uint32_t(it) & 1u;
@@ -1130,19 +1141,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
     __syncthreads();                   // every warp is done with the previous partition
     if (P.part_flag && threadIdx.x == 0) st_release_gpu(P.part_flag + (part - gridDim.x), ep);
   }
-  if (threadIdx.x == 0) {
-    next_chunk = 0;
-    next_er = 0;
-    next_comb = 0;
-    next_pcomb = 0;
-    if (P.pool_done)  // the next launch's counter of this partition
-      P.pool_done[((ep + 1u) & 1u) * uint32_t(P.n_parts) + uint32_t(part)] = 0u;
-  }
-  for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
-    chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
-  for (int i = threadIdx.x; i < kMaxErBuf / 32; i += blockDim.x) er_done[i] = 0u;
-  __syncthreads();
-
+  // the window copy first (every warp is done with the previous window)
   if (threadIdx.x == 0) {
     if constexpr (SMEM) {
       if (P.window_tma) {
@@ -1158,6 +1157,29 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
       }
     }
   }
+  if (threadIdx.x == 0) {
+    next_chunk = 0;
+    next_er = 0;
+    next_comb = 0;
+    next_pcomb = 0;
+    if (P.pool_done)  // the next launch's counter of this partition
+      P.pool_done[((ep + 1u) & 1u) * uint32_t(P.n_parts) + uint32_t(part)] = 0u;
+  }
+  for (int i = threadIdx.x; i < int((n_chunks + 31) >> 5); i += blockDim.x)
+    chunk_done[i] = P.do_ell ? 0u : 0xffffffffu;
+  for (int i = threadIdx.x; i < kMaxErBuf / 32; i += blockDim.x) er_done[i] = 0u;
+  if constexpr (C32) {
+    // the unit's chunk metadata, once: claims then read shared memory instead
+    // of an L2 round trip per chunk
+    if (P.meta_off >= 0 && P.do_ell) {
+      int2* sm = reinterpret_cast<int2*>(smem_raw + P.meta_off);
+      const int64_t sf = row0 >> 5;
+      for (int i = threadIdx.x; i < int(n_chunks); i += blockDim.x)
+        sm[i] = make_int2(__ldg(P.pos_ell + sf + i), __ldg(P.width_ell + sf + i));
+    }
+  }
+  __syncthreads();
+
   if constexpr (C32) {
     // warm L2 with the first slices of the partition's ELL stream
     if (P.do_ell && P.pf_ell > 0 && wid == 0) {
@@ -1257,9 +1279,15 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
     EllMeta m{0, 0};
     if (chunk < n_chunks) {
       if constexpr (C32) {
-        const int64_t s = (row0 >> 5) + chunk;
-        m.eff = __ldg(P.width_ell + s);
-        m.pos = __ldg(P.pos_ell + s);
+        if (P.meta_off >= 0) {
+          const int2 v = reinterpret_cast<const int2*>(smem_raw + P.meta_off)[chunk];
+          m.pos = v.x;
+          m.eff = v.y;
+        } else {
+          const int64_t s = (row0 >> 5) + chunk;
+          m.eff = __ldg(P.width_ell + s);
+          m.pos = __ldg(P.pos_ell + s);
+        }
         const int w = m.eff & kEffWidth;
         if (lane == 0 && P.pf_ell > 0 && w > 0)  // precise L2 prefetch of the claimed chunk
           prefetch_slice(P.val_ell, P.col_ell, int64_t(m.pos), int64_t(m.pos) + 32 * int64_t(w));
@@ -1315,7 +1343,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
         store = !((__ldg(P.long_bits + (row0 >> 5) + chunk) >> lane) & 1u);
       }
       publish();
-      if (store) P.y[row0 + chunk * 32 + lane] = acc;
+      if (store) y_lane[int(chunk) * 32] = acc;
       // only slices with an ER row are waited on (wait_chunk / own_pre)
       unpublished = (m.eff & kEffHasEr) ? chunk : -1;
     } else {
@@ -1534,7 +1562,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
     if constexpr (EHYB_ER_PAIRS && sizeof(T) == 4) {
     for (;;) {  // two own slices per claim (fp32: the pair fits the register budget)
       int v = 0;
-      if (lane == 0) v = atomicAdd(&next_er, 2);
+      if (lane == 0) v = atom_add_shared(&next_er, 2);
       const int64_t idx = __shfl_sync(0xffffffffu, v, 0);
       if (idx >= n_own) break;
       const ErMeta ma = er_meta(s0 + idx, s1), mb = er_meta(s0 + idx + 1, s1);
@@ -1572,7 +1600,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
     constexpr int kCs = sizeof(T) == 8 ? 2 : 1;  // fp32: one per claim (register budget)
     for (;;) {
       int v = 0;
-      if (lane == 0) v = atomicAdd(&next_comb, kCs);
+      if (lane == 0) v = atom_add_shared(&next_comb, kCs);
       const int64_t idx = __shfl_sync(0xffffffffu, v, 0);
       if (idx >= n_buf) break;
       const bool two = kCs == 2 && idx + 1 < n_buf;
@@ -1617,7 +1645,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
       constexpr int kPs = sizeof(T) == 8 ? 2 : 1;
       for (;;) {
         int v = 0;
-        if (lane == 0) v = atomicAdd(&next_pcomb, kPs);
+        if (lane == 0) v = atom_add_shared(&next_pcomb, kPs);
         const int64_t idx = __shfl_sync(0xffffffffu, v, 0);
         if (idx >= q1 - q0) break;
         const bool two = kPs == 2 && idx + 1 < q1 - q0;
