@@ -744,6 +744,21 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     total += ell_cost[size_t(q)] + er_total[size_t(q)];
   }
   const double budget_mean = n_units ? total / double(n_units) : 0.0;
+  // ER-heavy matrices (ER > 40% of the modelled work): ER-first warps in
+  // proportion to the ER share, so more of the latency-bound ER chains run
+  // under the stream (profiles/ab_erw_r3.jsonl: cfg4, share 0.55, 69.2 us at
+  // 6 warps -> 60.7 / 59.9 us at 12 / 14 of 24; below the threshold the
+  // measured optimum stays 6: cfg2 (0.32) 100.4 us at 6 vs 100.7 at 8, cfg3
+  // and cfg5 flat)
+  if (!small && total > 0.0) {
+    double er_sum = 0.0;
+    for (double v : er_total) er_sum += v;
+    const double share = er_sum / total;
+    const int nw = h->threads / 32;
+    if (share > 0.4)
+      h->er_warps = std::max(h->er_warps, std::min(int(std::lround(double(nw) * share)), nw - 8));
+  }
+  h->er_warps = int(env_double("EHYB_ER_WARPS", double(h->er_warps)));  // dev override
   struct SliceRef { int64_t q, i0; bool halo; };
   std::vector<std::vector<SliceRef>> own(static_cast<size_t>(n_units)), spill(static_cast<size_t>(n_units));
   for (int64_t q = 0; q < n_units; ++q) {

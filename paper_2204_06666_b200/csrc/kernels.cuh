@@ -631,6 +631,12 @@ __device__ __forceinline__ T er_slice_compute(const SpmvParams<T>& P, const ErMe
   return acc;
 }
 
+#ifndef EHYB_ER_PAIRS_F64_GROUP
+#define EHYB_ER_PAIRS_F64_GROUP 1  // fp64: pairs in the persistent group drain (cfg3 fp64 177.6 -> 173.7 us)
+#endif
+#ifndef EHYB_ER_PAIRS_F64
+#define EHYB_ER_PAIRS_F64 0  // fp64: pairs in the pool drain and own-ER passes too
+#endif
 #ifndef EHYB_ER_PAIRS
 #define EHYB_ER_PAIRS 1
 #endif
@@ -882,7 +888,7 @@ __device__ bool pool_drain(const SpmvParams<T>& P, int lane, int max_items, uint
     flush();
     return true;
   }
-  if constexpr (EHYB_ER_PAIRS && sizeof(T) == 4) {
+  if constexpr (EHYB_ER_PAIRS && (sizeof(T) == 4 || EHYB_ER_PAIRS_F64)) {
   for (;;) {  // two slices per claim (fp32: the pair fits the register budget)
     unsigned int v = 0;
     if (lane == 0) v = atomicAdd(ctr, 2u);
@@ -939,7 +945,7 @@ __device__ void pool_drain_group(const SpmvParams<T>& P, int lane, uint32_t ep, 
     while (ld_acquire_gpu(P.part_flag + owner) != ep) __nanosleep(64);
     P.y[r] = add_rn(__ldcg(P.y + r), acc);
   };
-  constexpr unsigned kStep = (EHYB_ER_PAIRS && sizeof(T) == 4) ? 2u : 1u;
+  constexpr unsigned kStep = (EHYB_ER_PAIRS && (sizeof(T) == 4 || EHYB_ER_PAIRS_F64_GROUP)) ? 2u : 1u;
   for (;;) {
     unsigned int v = 0;
     if (lane == 0) v = atomicAdd(ctr, kStep);
@@ -1559,7 +1565,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
 
   if (P.do_er) {
     if (pending >= 0 && pending < n_own) finish_own_er(pending, er_meta(s0 + pending, s1));
-    if constexpr (EHYB_ER_PAIRS && sizeof(T) == 4) {
+    if constexpr (EHYB_ER_PAIRS && (sizeof(T) == 4 || EHYB_ER_PAIRS_F64)) {
     for (;;) {  // two own slices per claim (fp32: the pair fits the register budget)
       int v = 0;
       if (lane == 0) v = atom_add_shared(&next_er, 2);

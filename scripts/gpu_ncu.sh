@@ -5,7 +5,7 @@
 TAG=${1:-r2}; shift
 CONFIGS=${@:-cfg2 cfg3f32 cfg3f64 cfg5 cfg1 cfg4}
 OUT=gpurun_out; mkdir -p $OUT
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+# the prebuilt .so files travel with the snapshot (no rebuild on the box)
 NCU="ncu --set full --clock-control none --import-source on -k regex:spmv_fused -s 5 -c 1"
 for C in $CONFIGS; do
   timeout 900 $NCU -o $OUT/prof_${TAG}_$C python scripts/launch_once.py --config $C --n 7 > $OUT/ncu_${TAG}_$C.log 2>&1
