@@ -135,19 +135,27 @@ def build_workload(name: str):
     nw, rw, cw, vw = W.stencil27(8, 8, 8)
     E.build_ehyb_gpu(E.CooMatrix(nw, nw, rw, cw, vw), tau=tau, profile=E.DeviceProfile(4, 32, 8192),
                      device=0)
-    t = {}
-    t0 = time.perf_counter()
-    e = E.build_ehyb_gpu(m, tau=tau, profile=E.DeviceProfile(*prof) if prof else E.B200_PROFILE,
-                         device=0, timings=t)
-    total = time.perf_counter() - t0
+    # the first build of a large matrix also pays one-time allocations
+    # (process-wide pinned staging, device scratch): reported as first_call;
+    # the timings are of a second, steady-state build of the same matrix
+    t, first = {}, None
+    for rep in range(2 if os.environ.get("EHYB_BENCH_PREP_REPEAT", "1") != "0" else 1):
+        t = {}
+        t0 = time.perf_counter()
+        e = E.build_ehyb_gpu(m, tau=tau, profile=E.DeviceProfile(*prof) if prof else E.B200_PROFILE,
+                             device=0, timings=t)
+        total = time.perf_counter() - t0
+        if rep == 0:
+            first = dict(t, total_s=total)
     assert e.params == params
-    return m, e, dict(generate_s=t_gen,
+    return m, e, dict(generate_s=t_gen, first_call=first,
                       partition_s=t["upload_s"] + t["build_graph_s"] + t["partition_graph_s"],
                       reorder_assemble_s=t["reorder_assemble_s"], upload_s=t["upload_s"],
                       build_graph_s=t["build_graph_s"], partition_graph_s=t["partition_graph_s"],
                       total_s=total, where="GPU (build_graph, classify/reorder/assemble) + host "
                                            "(BFS partition_graph); kernel modules loaded "
-                                           "beforehand (one-time lazy-loading cost excluded)")
+                                           "beforehand (one-time lazy-loading cost excluded); "
+                                           "steady state = the second build of the matrix")
 
 
 def golden_y_digest(name: str):

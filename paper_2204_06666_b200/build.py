@@ -34,9 +34,25 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+STAMP = LIB + ".flags"  # the dev flags the library was built with ("" = the product build)
+
+
+def _built_flags() -> str | None:
+    try:
+        with open(STAMP) as fh:
+            return fh.read()
+    except OSError:
+        return None
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
-    if os.environ.get("EHYB_NVCC_FLAGS"):
+    flags = os.environ.get("EHYB_NVCC_FLAGS", "")
+    if flags:
+        force = True
+    # a library left by a dev experiment (EHYB_NVCC_FLAGS, e.g. a one-variant
+    # build) is never taken for the product build
+    if _built_flags() != flags:
         force = True
     if not force and not _stale(LIB, deps):
         return LIB
@@ -57,6 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(proc.stderr)
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(flags)
     return LIB
 
 

@@ -761,10 +761,14 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   h->er_warps = int(env_double("EHYB_ER_WARPS", double(h->er_warps)));  // dev override
   struct SliceRef { int64_t q, i0; bool halo; };
   std::vector<std::vector<SliceRef>> own(static_cast<size_t>(n_units)), spill(static_cast<size_t>(n_units));
+  // persistent CTAs: units of the last iteration may keep a different share
+  // (their pooled slices can only be finished after the loop)
+  const int64_t last_it0 = n_units > h->max_ctas ? (n_units - 1) / h->max_ctas * h->max_ctas : n_units;
+  const double pool_factor_last = env_double("EHYB_POOL_FACTOR_LAST", pool_factor);
   for (int64_t q = 0; q < n_units; ++q) {
     const auto& mem = members[size_t(q)];
-    double left = (pool_ok && pool_factor > 0.0) ? pool_factor * budget_mean - ell_cost[size_t(q)]
-                                                 : 1e300;
+    const double pf = q >= last_it0 ? pool_factor_last : pool_factor;
+    double left = (pool_ok && pf > 0.0) ? pf * budget_mean - ell_cost[size_t(q)] : 1e300;
     bool spilling = false;
     for (size_t i0 = 0; i0 < mem.size(); i0 += 32) {
       double c = 0.0;
