@@ -116,6 +116,8 @@ struct ehyb_dev {
   unsigned int* pool_done = nullptr;
   int32_t* pool_own_ptr = nullptr;
   int32_t* pool_own_idx = nullptr;
+  int32_t* unit_part = nullptr;  // persistent launches: unit -> partition (heaviest first)
+  int32_t* part_unit = nullptr;  // its inverse
   void* pool_acc = nullptr;
   int32_t* pool_pos = nullptr;   // owner-major position of each pooled slice
   int32_t* pool_rows = nullptr;  // pooled slices' rows, owner-major
@@ -184,7 +186,7 @@ struct ehyb_dev {
   ~ehyb_dev() {
     void* ptrs[] = {val_ell, col_ell, pos_ell, width_ell, er_part_ptr, er_part_mid, er_pos, er_swidth,
                     er_rows, er_lwidth, er_val, er_col, reorder, inverse, xr, yr, xu, yu,
-                    pool_done, pool_own_ptr, pool_own_idx, pool_acc, pool_pos, pool_rows, own_acc, p2p_x, p2p_flags, pull_src, pull_off, peer_x_dev, peer_flags_dev,
+                    pool_done, pool_own_ptr, pool_own_idx, unit_part, part_unit, pool_acc, pool_pos, pool_rows, own_acc, p2p_x, p2p_flags, pull_src, pull_off, peer_x_dev, peer_flags_dev,
                     pool_ctr, epoch_dev, part_flag, pool_grp, pool_gctr,
                     part_stage_ptr, st_pos, st_slots, st_chunks, ch_stage,
                     bx[2], by[2], bx[0], bx[1], by[0], by[1], long_bits, lr_span,
@@ -270,6 +272,8 @@ cudaError_t launch_typed(const ehyb_dev* h, const void* x, void* y, bool do_ell,
   P.split = h->split;
   P.unit_chunks = h->unit_chunks;
   P.meta_off = h->meta_off;
+  P.unit_part = h->unit_part;
+  P.part_unit = h->part_unit;
   P.ell_ahead = h->ell_ahead;
   P.er_ahead = h->er_ahead;
   P.long_bits = h->long_bits;
@@ -713,6 +717,36 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
     }
   }
 
+  // persistent launches (more units than resident CTAs, one unit per
+  // partition), EHYB_ORDER_UNITS=1: units run in decreasing modelled cost
+  // (ELL slots + er_cost * ER entries), so the last iteration holds the
+  // lightest partitions. A derived launch order only (rows, x and y keep the
+  // reference layout; bitwise the same y). Measured off by default
+  // (profiles/ab_order_r3.jsonl: cfg3 fp64 172.0 vs 172.2 us, cfg5 978 vs 967)
+  std::vector<int32_t> upart;
+  if (split == 1 && C == 32 && n_units > h->max_ctas && env_double("EHYB_ORDER_UNITS", 0.0) != 0.0) {
+    const double ec = env_double("EHYB_ER_COST", 5.0);
+    std::vector<double> cost(static_cast<size_t>(n_units), 0.0);
+    for (int64_t q = 0; q < n_units; ++q) {
+      const int64_t a = (q * vec) / C, b = ((q + 1) * vec) / C;
+      cost[size_t(q)] = double(pos[size_t(b)] - pos[size_t(a)]);
+      for (int64_t j : members[size_t(q)]) cost[size_t(q)] += ec * m->er_row_widths[j];
+    }
+    upart.resize(static_cast<size_t>(n_units));
+    for (int64_t q = 0; q < n_units; ++q) upart[size_t(q)] = int32_t(q);
+    std::stable_sort(upart.begin(), upart.end(),
+                     [&](int32_t a, int32_t b) { return cost[size_t(a)] > cost[size_t(b)]; });
+    for (auto* grp : {&members, &hmembers}) {
+      std::vector<std::vector<int64_t>> by_unit(static_cast<size_t>(n_units));
+      for (int64_t u = 0; u < n_units; ++u) by_unit[size_t(u)].swap((*grp)[size_t(upart[size_t(u)])]);
+      grp->swap(by_unit);
+    }
+    std::vector<int32_t> pu(static_cast<size_t>(n_units));
+    for (int64_t u = 0; u < n_units; ++u) pu[size_t(upart[size_t(u)])] = int32_t(u);
+    CUDA_TRY(upload(&h->unit_part, upart.data(), upart.size() * 4, &h->bytes));
+    CUDA_TRY(upload(&h->part_unit, pu.data(), pu.size() * 4, &h->bytes));
+  }
+
   // per-partition 32-row ER slices (members in reference order), then the
   // own / pool split: partition q keeps the prefix of its ER slices that fits
   // its share of the mean per-CTA cost (ELL slots + er_cost * ER entries);
@@ -736,7 +770,8 @@ int create_impl(const ehyb_host_matrix* m, int64_t p0, int64_t p1, const int64_t
   std::vector<double> ell_cost(static_cast<size_t>(n_units)), er_total(static_cast<size_t>(n_units), 0.0);
   double total = 0.0;
   for (int64_t q = 0; q < n_units; ++q) {
-    const int64_t qp = q / split, c0 = (q % split) * unit_chunks;
+    const int64_t qp = upart.empty() ? q / split : int64_t(upart[size_t(q)]),
+                  c0 = (q % split) * unit_chunks;
     const int64_t a = (qp * vec) / C + c0 * (32 / C),
                   b = std::min<int64_t>(((qp + 1) * vec) / C, a + unit_chunks * (32 / C));
     ell_cost[size_t(q)] = double(pos[size_t(b)] - pos[size_t(a)]);

@@ -135,6 +135,8 @@ struct SpmvParams {
   const int32_t* __restrict__ st_slots;
   const int32_t* __restrict__ st_chunks;
   const uint2* __restrict__ ch_stage;          // [local_rows/32]
+  const int32_t* __restrict__ unit_part;  // persistent launches: partition of each unit (null =
+  const int32_t* __restrict__ part_unit;  // identity; units run heaviest first) and its inverse
   int32_t meta_off;                 // >= 0: byte offset in dynamic smem of the unit's chunk
                                     // metadata {pos, eff} (loaded once per partition; the
                                     // per-chunk claims then read shared memory), -1 = global
@@ -164,7 +166,7 @@ struct SpmvParams {
 template <bool SPLIT, typename T>
 __device__ __forceinline__ uint32_t unit_of_row(const SpmvParams<T>& P, uint32_t r) {
   const uint32_t q = r / uint32_t(P.vec);
-  if constexpr (!SPLIT) return q;
+  if constexpr (!SPLIT) return P.part_unit ? uint32_t(__ldg(P.part_unit + q)) : q;
   const uint32_t h = ((r - q * uint32_t(P.vec)) >> 5) / uint32_t(P.unit_chunks);
   return q * uint32_t(P.split) + (h < uint32_t(P.split) ? h : uint32_t(P.split) - 1u);
 }
@@ -1129,7 +1131,7 @@ __global__ void __launch_bounds__(max_threads_for(int(sizeof(T))), 1)
   // unit `part` = chunks [c0, c0 + n_chunks) of partition q; row0 is the
   // unit's first row, the window is the whole partition's
   // (SPLIT: compiled only into the variant launched when split > 1)
-  const int64_t q = SPLIT ? part / P.split : part;
+  const int64_t q = SPLIT ? part / P.split : (P.unit_part ? int64_t(__ldg(P.unit_part + part)) : part);
   const int64_t c0 = SPLIT ? int64_t(part - q * P.split) * P.unit_chunks : 0;
   const int64_t n_chunks =
       SPLIT ? (part_chunks - c0 < P.unit_chunks ? part_chunks - c0 : P.unit_chunks) : part_chunks;

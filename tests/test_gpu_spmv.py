@@ -455,3 +455,33 @@ def test_work_units_split_partitions(monkeypatch, split, tau):
                 A.spmv_local(x_ext, ys, exact=True)
                 torch.cuda.synchronize()
                 assert ys.cpu().numpy().tobytes() == want[lo:hi].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tau", [8, 4])
+@pytest.mark.parametrize("knobs", [
+    {"EHYB_META_SMEM": "0"}, {"EHYB_META_SMEM": "1"},
+    {"EHYB_ORDER_UNITS": "1"}, {"EHYB_ORDER_UNITS": "1", "EHYB_META_SMEM": "1"},
+    {"EHYB_ER_WARPS": "12"}, {"EHYB_POOL_FACTOR_LAST": "1.2"},
+])
+def test_launch_layout_knobs_keep_y_bitwise(monkeypatch, knobs, tau):
+    # derived launch layouts (chunk metadata in shared memory, units in cost
+    # order with their unit -> partition table, ER-first warp count, the last
+    # iteration's pool share) change only where and when rows are computed:
+    # y stays bitwise the reference restatement's, one wave and persistent
+    n, r, c, v = W.permute_symmetric(*W.stencil27(40, 40, 40), seed=5)
+    m = E.CooMatrix(n, n, r, c, v)
+    x = W.deterministic_vector(n, 7)
+    for k, val in knobs.items():
+        monkeypatch.setenv(k, val)
+    for prof in (E.DeviceProfile(600, 32, 4096), E.DeviceProfile(64, 32, 4096)):
+        e = E.build_ehyb(m, tau=tau, profile=prof)
+        xr = E.permute_vector(x, e.plan).astype(e.params.value_dtype)
+        want = c_oracle.spmv_ehyb(e, xr)
+        dm = E.device_matrix(e, 0)
+        xt = torch.from_numpy(xr).to("cuda:0")
+        for _ in range(2):
+            y = dm.spmv(xt)
+            torch.cuda.synchronize()
+            assert y.cpu().numpy().tobytes() == want.tobytes()
+        dm.close()
