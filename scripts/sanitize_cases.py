@@ -45,6 +45,20 @@ def main():
     xr = E.permute_vector(W.deterministic_vector(n, 6), e.plan)
     y, _ = E.spmv_ehyb(e, xr)
     ok &= check("persistent", y, c_oracle.spmv_ehyb(e, xr))
+    # 2b. fp32 one-wave (chunk metadata in shared memory, paired ER slices)
+    # and persistent CTAs in cost order (unit -> partition table)
+    n, r, c, v = W.permute_symmetric(*W.stencil27(20, 20, 20), seed=3)
+    e = E.build_ehyb(E.CooMatrix(n, n, r, c, v), tau=4, profile=E.DeviceProfile(16, 32, 8192))
+    xr = E.permute_vector(W.deterministic_vector(n, 1), e.plan).astype(np.float32)
+    y, _ = E.spmv_ehyb(e, xr)
+    ok &= check("fp32 metadata in smem", y, c_oracle.spmv_ehyb(e, xr))
+    os.environ["EHYB_ORDER_UNITS"] = "1"
+    n, r, c, v = W.permute_symmetric(*W.stencil27(24, 24, 24), seed=5)
+    e = E.build_ehyb(E.CooMatrix(n, n, r, c, v), tau=8, profile=E.DeviceProfile(300, 32, 2048))
+    xr = E.permute_vector(W.deterministic_vector(n, 6), e.plan)
+    y, _ = E.spmv_ehyb(e, xr)
+    ok &= check("persistent, cost-ordered units", y, c_oracle.spmv_ehyb(e, xr))
+    del os.environ["EHYB_ORDER_UNITS"]
     # 3. long rows, strict / default / fma
     n, r, c, v = W.heavy_tail(k=12, n_hubs=3, min_len=200, max_len=2000)
     e = E.build_ehyb(E.CooMatrix(n, n, r, c, v), tau=8, profile=E.DeviceProfile(16, 32, 8192))
