@@ -462,7 +462,11 @@ def run_gpu(args):
     bmin = E.min_bytes(e)
     gold = golden_y_digest(args.config)
 
-    dm = E.device_matrix(e, dev)
+    t0 = time.perf_counter()
+    dm = E.device_matrix(e, dev)  # upload + derived device layout (ehyb_dev_create)
+    torch.cuda.synchronize(dev)
+    prep_t["device_matrix_s"] = time.perf_counter() - t0
+    prep_t["device_matrix_gbytes"] = dm.info()["device_bytes"] / 1e9
     info = dm.info()
     stream = torch.cuda.Stream(dev)
     x = W.deterministic_vector(e.dimension, 0)

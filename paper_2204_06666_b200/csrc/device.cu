@@ -65,7 +65,13 @@ cudaError_t upload(P** dst, const void* src, size_t bytes, size_t* total) {
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), std::max<size_t>(bytes, 16));
   if (e != cudaSuccess) return e;
   *total += std::max<size_t>(bytes, 16);
-  if (bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  // large arrays (the ELL slab: 4.5 GB for cfg5) through the pinned double
+  // buffer: host copy of one half overlapped with the DMA of the other
+  static const bool staged = [] {
+    const char* v = std::getenv("EHYB_UPLOAD_STAGED");  // dev: 0 = plain cudaMemcpy
+    return !(v && *v && std::atof(v) == 0.0);
+  }();
+  if (bytes) e = staged ? staged_h2d(*dst, src, bytes) : cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
   return e;
 }
 

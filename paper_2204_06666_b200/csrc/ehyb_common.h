@@ -19,6 +19,11 @@ inline int fail(const std::string& msg, int code = EHYB_EINVAL) {
 }
 inline int fail_oom() { return fail("out of host memory", EHYB_ENOMEM); }
 
+#ifdef __CUDACC__
+// prep_gpu.cu: pageable -> device copy through the pinned staging buffers
+cudaError_t staged_h2d(void* dev, const void* host, size_t bytes);
+#endif
+
 }  // namespace ehyb
 
 #define EHYB_TRY try

@@ -391,6 +391,16 @@ __global__ void k_place(const int64_t* __restrict__ rptr, const int32_t* __restr
 
 }  // namespace
 
+namespace ehyb {
+// pageable host -> device copy of a large array through the process-wide
+// pinned double buffer (device.cu: the device-matrix upload); small copies
+// go straight through cudaMemcpy
+cudaError_t staged_h2d(void* dev, const void* host, size_t bytes) {
+  Staging st;
+  return st.h2d(dev, host, bytes);
+}
+}  // namespace ehyb
+
 struct ehyb_gprep {
   int device = 0;
   Staging stage;
